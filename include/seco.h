@@ -1,0 +1,135 @@
+/*
+ * seco.h -- C ABI of libseco.so: the data-parallel hot path of SeCO / SpaCO
+ * (Sequential / Sparse Chunk-wise Optimization, arXiv 2505.16710) for one
+ * causal GQA attention layer on NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = PAPER.md line n.  The operations follow the paper's
+ * problem statement: a sequence of k chunks of size c (Eq. 1);
+ * chunk j's forward reads the KV cache of all earlier chunks (Eq. 1, Alg. 1
+ * line 2 P:196); the chunk-local backward runs in reverse chunk order and
+ * deposits gradients into every preceding checkpoint (Alg. 1
+ * lines 4-7 P:199-202); SpaCO samples t of the k chunks and scales the relayed
+ * checkpoint gradient by the compensation factor k/t (Alg. 2, capped
+ * per P:415).
+ *
+ * Conventions (readings Z1-Z4 of DESIGN.md §3):
+ *   - chunk index j is 0-based; query row r of chunk j is at absolute position
+ *     p = j*c + r and sees every key position q <= p (cache slots 0..j-1 fully,
+ *     its own slot j causally);
+ *   - q-head h reads kv-head g = h / (hq/hkv);
+ *   - logits are softmax_scale * <q, k>, softmax_scale <= 0 means 1/sqrt(d);
+ *   - LSE is the natural-log log-sum-exp of the scaled logits, float32.
+ *
+ * Layouts (all row-major, innermost dimension d contiguous, strides in ELEMENTS):
+ *   q, o, d_o, dq : [hq][c][d]   element (h, r, x) at h*q_head_stride + r*q_row_stride + x
+ *   k_cache, v_cache : [hkv][S][d], S = c*num_chunks, element (g, q, x) at
+ *                  g*kv_head_stride + q*kv_row_stride + x; slot j = rows [j*c, (j+1)*c)
+ *   lse           : [hq][c] float32, dense
+ *   dkv           : [2][hkv][S][d] float32, dense (index 0 = dK, 1 = dV): the
+ *                   persistent checkpoint-gradient buffer m'.grad
+ *   dk_own, dv_own: [hkv][c][d], dense, same element type as q
+ * Element type: bf16 for SECO_BF16, float32 for SECO_FP32_DEBUG.
+ *
+ * Ownership: the caller owns every buffer (device memory), including dkv, which
+ * the caller zeroes once per training step.  The library never allocates device
+ * memory, never synchronises, and enqueues all work on `stream`.  Host-side
+ * state: a mutex-guarded cache of kernel attributes only.  All functions are
+ * reentrant.
+ *
+ * Errors: return codes only, nothing throws across the ABI.  Arguments are
+ * validated on the host before any launch (SECO_ERR_ARG: null pointer, j out of
+ * range, hq % hkv != 0, non-positive sizes, misaligned pointer or stride;
+ * SECO_ERR_UNSUPPORTED: a shape the bf16 tensor-core path does not implement --
+ * it needs d in {64, 128}, c % 128 == 0, 16-byte aligned rows; the fp32 debug
+ * path accepts any d <= 256 and any c).  Launch failures return SECO_ERR_CUDA;
+ * faults during execution surface at the caller's next synchronisation.
+ */
+#ifndef SECO_H_
+#define SECO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* seco_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum { SECO_OK = 0, SECO_ERR_ARG = 1, SECO_ERR_UNSUPPORTED = 2, SECO_ERR_CUDA = 3 } seco_status;
+typedef enum { SECO_BF16 = 0, SECO_FP32_DEBUG = 1 } seco_dtype;
+typedef enum { SPACO_PAPER = 0, SPACO_HT = 1, SPACO_BERNOULLI = 2 } spaco_mode;
+
+typedef struct {
+  int32_t hq, hkv, d;       /* q heads, kv heads, head dim                        */
+  int32_t chunk;            /* c: rows per chunk (the paper's chunk size)         */
+  int32_t num_chunks;       /* k: number of chunks, S = c * k                     */
+  float softmax_scale;      /* <= 0 -> 1/sqrt(d)                                  */
+  seco_dtype dtype;
+  int64_t q_head_stride, q_row_stride;   /* for q, o, d_o, dq                     */
+  int64_t kv_head_stride, kv_row_stride; /* for k_cache, v_cache                  */
+} seco_shape;
+
+/* Bytes of device workspace `ws` the two chunk calls need (dQ accumulator,
+ * row statistics).  Same for every j. */
+size_t seco_workspace_size(const seco_shape* shape);
+
+/* Chunk forward (Eq. 1; Alg. 1 lines 2 and 5): for the c
+ * query rows of chunk j, attend to cache slots 0..j (own slot causally) with
+ * an online softmax; write O_j (o) and LSE_j (lse).  Slot j of k_cache/v_cache
+ * must already hold chunk j's keys/values.  Deterministic: the stage-2 rebuild
+ * reproduces stage 1 bit for bit.  `ws` may be NULL when
+ * seco_workspace_size() == 0 is not required by the chosen schedule. */
+seco_status seco_chunk_forward(const seco_shape* shape, int32_t j,
+                               const void* q, const void* k_cache, const void* v_cache,
+                               void* o, float* lse,
+                               void* ws, size_t ws_bytes, seco_stream_t stream);
+
+/* Chunk-local backward (Alg. 1 lines 6-7 P:200-201; Alg. 2 lines 6-7
+ * P:334-335; relay = grad_hook(grad, base, scaler) P:551-552).  Inputs: the
+ * chunk's q, o (from seco_chunk_forward), d_o (cotangent of o), lse.  Effects,
+ * with s = grad_scale (loss seed scale; 1 for SeCO and Alg. 2 as printed) and
+ * gamma = relay_scale (1 for SeCO, the compensation factor for SpaCO):
+ *   dq                    = s * dQ_j                          (overwritten)
+ *   dkv[:, :, slot i < j] += s * dK^(j->i), s * dV^(j->i)     (deposits into earlier checkpoints)
+ *   dkv[:, :, slot j]      = gamma * dkv[:, :, slot j] + s * dK^(j->j)   (relay + own block)
+ *   dk_own, dv_own         = dkv[0|1, :, slot j] converted to the element type (skipped if NULL)
+ * Preconditions: every later chunk's backward that should deposit into slot j
+ * was enqueued earlier on `stream` (descending order, reading Z10).  Summation
+ * order of the fp32 deposits is not fixed (atomics; reading Z14). */
+seco_status seco_chunk_backward(const seco_shape* shape, int32_t j,
+                                const void* q, const void* k_cache, const void* v_cache,
+                                const void* o, const void* d_o, const float* lse,
+                                float relay_scale, float grad_scale,
+                                float* dkv, void* dq, void* dk_own, void* dv_own,
+                                void* ws, size_t ws_bytes, seco_stream_t stream);
+
+/* SpaCO sampling (Alg. 2 line 4 P:329 "Randomly select t distinct indices") and
+ * scales (cap P:415), on the host, integer-only PRNG (splitmix64, state =
+ * seed).  Writes the selected 0-based chunk indices strictly descending into
+ * idx_out (capacity k), their count into *n_out, the relay scale gamma into
+ * *relay_scale_out and the loss seed scale s into *seed_scale_out:
+ *   SPACO_PAPER:     t distinct (partial Fisher-Yates), gamma = min(k/t, cap), s = 1
+ *   SPACO_HT:        t distinct,                        gamma = (k-1)/(t-1), s = k/t
+ *   SPACO_BERNOULLI: i kept iff floor(u*k/2^64) < t,    gamma = s = k/t
+ * cap <= 0 disables the cap (applies to gamma in every mode).  Ratios are
+ * computed in double and rounded once to float.  Errors: SECO_ERR_ARG for null
+ * outputs, k < 1, t < 1, t > k, or SPACO_HT with t < 2. */
+seco_status spaco_sample_and_scale(int32_t k, int32_t t, uint64_t seed, float cap, spaco_mode mode,
+                                   int32_t* idx_out, int32_t* n_out,
+                                   float* relay_scale_out, float* seed_scale_out);
+
+/* Static string for a status code (never NULL). */
+const char* seco_status_string(seco_status status);
+
+/* Human-readable description of the most recent error on the calling thread. */
+const char* seco_last_error(void);
+
+/* Number of kernel launches the most recent successful chunk call on the
+ * calling thread enqueued (for launch accounting in the benchmark). */
+int32_t seco_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SECO_H_ */

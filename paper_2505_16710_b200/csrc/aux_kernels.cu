@@ -1,0 +1,353 @@
+// Memory-bound helper kernels of the chunk backward, shared by the bf16 and the
+// fp32-debug paths, and the fp32 SIMT "debug" forward/backward kernels.
+//
+//   bwd_prep   : D_j = rowsum(dO_j o O_j)  [hq][c] fp32;
+//                relay: dkv[:, :, slot j] *= gamma  (Alg. 2 line 6 P:334; grad_hook P:551 --
+//                the relayed checkpoint gradient is pre-scaled so that the own-slot
+//                deposits of the main kernel complete "grad + base * scaler");
+//                zero the fp32 dQ accumulator.
+//   bwd_final  : dQ_j = T(s * sigma * dQacc) and dk_own/dv_own = T(dkv[:, :, slot j]).
+//   fwd_fp32 / bwd_fp32_dq / bwd_fp32_dkv : plain FFMA reference kernels for the
+//                SECO_FP32_DEBUG dtype (any d <= 256, any chunk size).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace seco {
+
+template <typename T> SECO_DEV float ldf(const T* p);
+template <> SECO_DEV float ldf<float>(const float* p) { return *p; }
+template <> SECO_DEV float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <typename T> SECO_DEV void stf(T* p, float v);
+template <> SECO_DEV void stf<float>(float* p, float v) { *p = v; }
+template <> SECO_DEV void stf<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+SECO_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct PrepArgs {
+  int hq, hkv, c, d, j, S;
+  int64_t qh, qr;
+  float relay;
+  int nD, nR, nZ;  // block counts of the three tasks
+};
+
+// Task A (blocks [0,nD)): one warp per (h, row): D = sum_x dO*O.
+// Task B (blocks [nD,nD+nR)): scale slot j of dkv (both dK and dV) by relay.
+// Task C (rest): zero dQacc [hq][c][d].
+template <typename T>
+__global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, const T* __restrict__ d_o,
+                                                       float* __restrict__ D, float* __restrict__ dkv,
+                                                       float* __restrict__ dqacc, PrepArgs a) {
+  const int bid = blockIdx.x;
+  if (bid < a.nD) {
+    const int w = bid * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (w >= a.hq * a.c) return;
+    const int h = w / a.c, r = w % a.c;
+    const T* orow = o + (int64_t)h * a.qh + (int64_t)r * a.qr;
+    const T* drow = d_o + (int64_t)h * a.qh + (int64_t)r * a.qr;
+    float acc = 0.f;
+    for (int x = lane; x < a.d; x += 32) acc += ldf(orow + x) * ldf(drow + x);
+    acc = warp_sum(acc);
+    if (lane == 0) D[(int64_t)h * a.c + r] = acc;
+  } else if (bid < a.nD + a.nR) {
+    if (a.relay == 1.f) return;
+    const int64_t per = (int64_t)a.c * a.d;                 // one slot of one head
+    const int64_t total = 2 * (int64_t)a.hkv * per / 4;     // float4 units
+    for (int64_t i = (int64_t)(bid - a.nD) * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)a.nR * blockDim.x) {
+      const int64_t e = i * 4;
+      const int64_t th = e / per, off = e % per;              // th = tensor*hkv + g
+      float4* p = reinterpret_cast<float4*>(dkv + th * (int64_t)a.S * a.d + (int64_t)a.j * per + off);
+      float4 v = *p;
+      v.x *= a.relay; v.y *= a.relay; v.z *= a.relay; v.w *= a.relay;
+      *p = v;
+    }
+  } else {
+    if (dqacc == nullptr) return;
+    const int64_t total = (int64_t)a.hq * a.c * a.d / 4;
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (int64_t)(bid - a.nD - a.nR) * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)a.nZ * blockDim.x)
+      reinterpret_cast<float4*>(dqacc)[i] = z;
+  }
+}
+
+struct FinalArgs {
+  int hq, hkv, c, d, j, S;
+  int64_t qh, qr;
+  float dq_scale;  // s * sigma
+  int nQ, nO;
+};
+
+// Task A (blocks [0,nQ)): dq = T(dq_scale * dqacc) (skipped when dqacc == null).
+// Task B: dk_own / dv_own = T(dkv slot j).
+template <typename T>
+__global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict__ dqacc, T* __restrict__ dq,
+                                                        const float* __restrict__ dkv, T* __restrict__ dk_own,
+                                                        T* __restrict__ dv_own, FinalArgs a) {
+  const int bid = blockIdx.x;
+  if (bid < a.nQ) {
+    if (dqacc == nullptr) return;
+    const int64_t total = (int64_t)a.hq * a.c * a.d;
+    for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < total; i += (int64_t)a.nQ * blockDim.x) {
+      const int64_t h = i / ((int64_t)a.c * a.d), rem = i % ((int64_t)a.c * a.d);
+      const int64_t r = rem / a.d, x = rem % a.d;
+      stf(dq + h * a.qh + r * a.qr + x, a.dq_scale * dqacc[i]);
+    }
+  } else {
+    if (dk_own == nullptr && dv_own == nullptr) return;
+    const int64_t per = (int64_t)a.c * a.d;
+    const int64_t total = 2 * (int64_t)a.hkv * per;
+    for (int64_t i = (int64_t)(bid - a.nQ) * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)a.nO * blockDim.x) {
+      const int64_t th = i / per, off = i % per;
+      const int t = (int)(th / a.hkv), g = (int)(th % a.hkv);
+      const float v = dkv[th * (int64_t)a.S * a.d + (int64_t)a.j * per + off];
+      T* dst = t == 0 ? dk_own : dv_own;
+      if (dst) stf(dst + (int64_t)g * per + off, v);
+    }
+  }
+}
+
+template <typename T>
+static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, float* D, float* dkv, float* dqacc,
+                               float relay, cudaStream_t st) {
+  PrepArgs a;
+  a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
+  a.qh = g.qh; a.qr = g.qr; a.relay = relay;
+  a.nD = (g.hq * g.c + 7) / 8;
+  a.nR = relay == 1.f ? 0 : 296;
+  a.nZ = dqacc ? 296 : 0;
+  bwd_prep_kernel<T><<<a.nD + a.nR + a.nZ, 256, 0, st>>>(o, d_o, D, dkv, dqacc, a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch_final(const ChunkGeom& g, const float* dqacc, T* dq, const float* dkv, T* dk_own,
+                                T* dv_own, float dq_scale, cudaStream_t st) {
+  FinalArgs a;
+  a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
+  a.qh = g.qh; a.qr = g.qr; a.dq_scale = dq_scale;
+  a.nQ = dqacc ? 296 : 0;
+  a.nO = (dk_own || dv_own) ? 148 : 0;
+  if (a.nQ + a.nO == 0) return cudaSuccess;
+  bwd_final_kernel<T><<<a.nQ + a.nO, 256, 0, st>>>(dqacc, dq, dkv, dk_own, dv_own, a);
+  return cudaGetLastError();
+}
+
+// bf16 path helpers, used by launch_bwd_sm100
+cudaError_t launch_prep_bf16(const ChunkGeom& g, const void* o, const void* d_o, float* D, float* dkv,
+                             float* dqacc, float relay, cudaStream_t st) {
+  return launch_prep<__nv_bfloat16>(g, reinterpret_cast<const __nv_bfloat16*>(o),
+                                    reinterpret_cast<const __nv_bfloat16*>(d_o), D, dkv, dqacc, relay, st);
+}
+cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, const float* dkv, void* dk_own,
+                              void* dv_own, float dq_scale, cudaStream_t st) {
+  return launch_final<__nv_bfloat16>(g, dqacc, reinterpret_cast<__nv_bfloat16*>(dq), dkv,
+                                     reinterpret_cast<__nv_bfloat16*>(dk_own),
+                                     reinterpret_cast<__nv_bfloat16*>(dv_own), dq_scale, st);
+}
+
+// ===================================================================== fp32 debug path
+struct DbgArgs {
+  int hq, hkv, G, c, d, j;
+  float scale;
+  int64_t qh, qr, kh, kr;
+};
+
+// one warp per query row; online softmax over the visible keys (FFMA, expf/logf)
+template <int DPL>
+__global__ void __launch_bounds__(256) fwd_fp32_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                       const float* __restrict__ v, float* __restrict__ o,
+                                                       float* __restrict__ lse, DbgArgs a) {
+  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32, h = blockIdx.y;
+  if (r >= a.c) return;
+  const int g = h / a.G, pos = a.j * a.c + r;
+  const float* qrow = q + (int64_t)h * a.qh + (int64_t)r * a.qr;
+  float qv[DPL], acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int x = lane + 32 * i;
+    qv[i] = x < a.d ? qrow[x] : 0.f;
+    acc[i] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  for (int key = 0; key <= pos; ++key) {
+    const float* krow = k + (int64_t)g * a.kh + (int64_t)key * a.kr;
+    const float* vrow = v + (int64_t)g * a.kh + (int64_t)key * a.kr;
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int x = lane + 32 * i;
+      if (x < a.d) s += qv[i] * krow[x];
+    }
+    s = warp_sum(s) * a.scale;
+    const float m_new = fmaxf(m, s);
+    const float alpha = expf(m - m_new), p = expf(s - m_new);
+    l = l * alpha + p;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int x = lane + 32 * i;
+      acc[i] = acc[i] * alpha + (x < a.d ? p * vrow[x] : 0.f);
+    }
+    m = m_new;
+  }
+  float* orow = o + (int64_t)h * a.qh + (int64_t)r * a.qr;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int x = lane + 32 * i;
+    if (x < a.d) orow[x] = acc[i] / l;
+  }
+  if (lane == 0) lse[(int64_t)h * a.c + r] = m + logf(l);
+}
+
+// dQ: one warp per query row
+template <int DPL>
+__global__ void __launch_bounds__(256) bwd_fp32_dq_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                          const float* __restrict__ v, const float* __restrict__ d_o,
+                                                          const float* __restrict__ lse, const float* __restrict__ D,
+                                                          float* __restrict__ dq, float gscale, DbgArgs a) {
+  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32, h = blockIdx.y;
+  if (r >= a.c) return;
+  const int g = h / a.G, pos = a.j * a.c + r;
+  const float* qrow = q + (int64_t)h * a.qh + (int64_t)r * a.qr;
+  const float* drow = d_o + (int64_t)h * a.qh + (int64_t)r * a.qr;
+  float qv[DPL], dv[DPL], acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int x = lane + 32 * i;
+    qv[i] = x < a.d ? qrow[x] : 0.f;
+    dv[i] = x < a.d ? drow[x] : 0.f;
+    acc[i] = 0.f;
+  }
+  const float L = lse[(int64_t)h * a.c + r], Dr = D[(int64_t)h * a.c + r];
+  for (int key = 0; key <= pos; ++key) {
+    const float* krow = k + (int64_t)g * a.kh + (int64_t)key * a.kr;
+    const float* vrow = v + (int64_t)g * a.kh + (int64_t)key * a.kr;
+    float s = 0.f, dp = 0.f;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int x = lane + 32 * i;
+      if (x < a.d) { s += qv[i] * krow[x]; dp += dv[i] * vrow[x]; }
+    }
+    s = warp_sum(s) * a.scale;
+    dp = warp_sum(dp);
+    const float p = expf(s - L), ds = p * (dp - Dr);
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int x = lane + 32 * i;
+      if (x < a.d) acc[i] += ds * krow[x];
+    }
+  }
+  float* out = dq + (int64_t)h * a.qh + (int64_t)r * a.qr;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int x = lane + 32 * i;
+    if (x < a.d) out[x] = gscale * a.scale * acc[i];
+  }
+}
+
+// dK/dV: one warp per key (kv-head g, key position in [0, (j+1)c)); loops over the
+// G q-heads of the group and the chunk's rows that see the key; adds the key's
+// contribution into dkv (slot j was pre-scaled by the relay factor in bwd_prep).
+template <int DPL>
+__global__ void __launch_bounds__(256) bwd_fp32_dkv_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                           const float* __restrict__ v, const float* __restrict__ d_o,
+                                                           const float* __restrict__ lse, const float* __restrict__ D,
+                                                           float* __restrict__ dkv, float gscale, int S, DbgArgs a) {
+  const int key = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32, g = blockIdx.y;
+  const int end = (a.j + 1) * a.c;
+  if (key >= end) return;
+  const float* krow = k + (int64_t)g * a.kh + (int64_t)key * a.kr;
+  const float* vrow = v + (int64_t)g * a.kh + (int64_t)key * a.kr;
+  float kv[DPL], vv[DPL], dk[DPL], dvv[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int x = lane + 32 * i;
+    kv[i] = x < a.d ? krow[x] : 0.f;
+    vv[i] = x < a.d ? vrow[x] : 0.f;
+    dk[i] = 0.f;
+    dvv[i] = 0.f;
+  }
+  const int r0 = key > a.j * a.c ? key - a.j * a.c : 0;  // first row of the chunk that sees `key`
+  for (int hh = 0; hh < a.G; ++hh) {
+    const int h = g * a.G + hh;
+    for (int r = r0; r < a.c; ++r) {
+      const float* qrow = q + (int64_t)h * a.qh + (int64_t)r * a.qr;
+      const float* drow = d_o + (int64_t)h * a.qh + (int64_t)r * a.qr;
+      float s = 0.f, dp = 0.f;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int x = lane + 32 * i;
+        if (x < a.d) { s += kv[i] * qrow[x]; dp += vv[i] * drow[x]; }
+      }
+      s = warp_sum(s) * a.scale;
+      dp = warp_sum(dp);
+      const float p = expf(s - lse[(int64_t)h * a.c + r]);
+      const float ds = p * (dp - D[(int64_t)h * a.c + r]);
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int x = lane + 32 * i;
+        if (x < a.d) { dk[i] += ds * qrow[x]; dvv[i] += p * drow[x]; }
+      }
+    }
+  }
+  float* pk = dkv + ((int64_t)g * S + key) * a.d;
+  float* pv = dkv + ((int64_t)(a.hkv + g) * S + key) * a.d;
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    const int x = lane + 32 * i;
+    if (x < a.d) {
+      pk[x] += gscale * a.scale * dk[i];
+      pv[x] += gscale * dvv[i];
+    }
+  }
+}
+
+static DbgArgs dbg_args(const ChunkGeom& g) {
+  DbgArgs a;
+  a.hq = g.hq; a.hkv = g.hkv; a.G = g.hq / g.hkv; a.c = g.c; a.d = g.d; a.j = g.j;
+  a.scale = g.scale; a.qh = g.qh; a.qr = g.qr; a.kh = g.kh; a.kr = g.kr;
+  return a;
+}
+
+
+cudaError_t launch_fwd_fp32(const ChunkGeom& g, const float* q, const float* k, const float* v, float* o,
+                            float* lse, cudaStream_t st) {
+  DbgArgs a = dbg_args(g);
+  dim3 grid((g.c + 7) / 8, g.hq);
+  if (g.d <= 32) fwd_fp32_kernel<1><<<grid, 256, 0, st>>>(q, k, v, o, lse, a);
+  else if (g.d <= 64) fwd_fp32_kernel<2><<<grid, 256, 0, st>>>(q, k, v, o, lse, a);
+  else if (g.d <= 128) fwd_fp32_kernel<4><<<grid, 256, 0, st>>>(q, k, v, o, lse, a);
+  else fwd_fp32_kernel<8><<<grid, 256, 0, st>>>(q, k, v, o, lse, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_fp32(const ChunkGeom& g, const float* q, const float* k, const float* v, const float* o,
+                            const float* d_o, const float* lse, float relay, float gscale, float* dkv, float* dq,
+                            float* dk_own, float* dv_own, float* ws_D, cudaStream_t st, int* launches) {
+  cudaError_t e = launch_prep<float>(g, o, d_o, ws_D, dkv, nullptr, relay, st);
+  if (e != cudaSuccess) return e;
+  DbgArgs a = dbg_args(g);
+  dim3 gq((g.c + 7) / 8, g.hq);
+  if (g.d <= 32) bwd_fp32_dq_kernel<1><<<gq, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dq, gscale, a);
+  else if (g.d <= 64) bwd_fp32_dq_kernel<2><<<gq, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dq, gscale, a);
+  else if (g.d <= 128) bwd_fp32_dq_kernel<4><<<gq, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dq, gscale, a);
+  else bwd_fp32_dq_kernel<8><<<gq, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dq, gscale, a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int S = g.c * g.k;
+  dim3 gk(((g.j + 1) * g.c + 7) / 8, g.hkv);
+  if (g.d <= 32) bwd_fp32_dkv_kernel<1><<<gk, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dkv, gscale, S, a);
+  else if (g.d <= 64) bwd_fp32_dkv_kernel<2><<<gk, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dkv, gscale, S, a);
+  else if (g.d <= 128) bwd_fp32_dkv_kernel<4><<<gk, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dkv, gscale, S, a);
+  else bwd_fp32_dkv_kernel<8><<<gk, 256, 0, st>>>(q, k, v, d_o, lse, ws_D, dkv, gscale, S, a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  e = launch_final<float>(g, nullptr, dq, dkv, dk_own, dv_own, 1.f, st);
+  *launches = 3 + ((dk_own || dv_own) ? 1 : 0);
+  return e;
+}
+
+}  // namespace seco

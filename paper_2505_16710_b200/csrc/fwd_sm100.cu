@@ -1,0 +1,314 @@
+// Chunk forward on sm_100a tensor cores: O_j, LSE_j of chunk j against KV-cache
+// slots 0..j (Eq. 1; Alg. 1 lines 2 and 5), bf16 in, fp32
+// accumulate, online softmax.
+//
+// One CTA = one 128-row query tile of chunk j for NH q-heads of the same kv-head
+// group (GQA: the NH tiles share every K/V tile loaded into shared memory).
+// Warp roles (warp-uniform dispatch):
+//   warp 0        TMA producer: Q tiles once, then K_t, V_t through a STAGES-deep ring
+//   warp 1        MMA issuer (one thread): S_b = Q_b K_t^T and O_b += P_b V_t (tcgen05.mma)
+//   warp 2        TMEM allocator
+//   warps 4..     one 128-thread softmax warpgroup per q-head tile b (thread = query row):
+//                 tcgen05.ld S_b, online softmax in the log2 domain, P_b -> smem (bf16,
+//                 128B swizzle), lazy O rescale in TMEM, epilogue O/l -> global, LSE.
+// MMA issue order ping-pongs the NH tiles: PV_0(t), S_0(t+1), PV_1(t), S_1(t+1), ...
+// so softmax of one tile overlaps tensor-core work of the other.
+// TMEM: S_b at columns [128b, 128b+128), O_b at [128 NH + D b, ... + D).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace seco {
+
+namespace fwd {
+constexpr int BM = 128;  // query rows per tile (= UMMA M)
+constexpr int BN = 128;  // keys per K/V tile (= UMMA N of S, K of PV)
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
+
+template <int NH, int D, int STAGES>
+struct Layout {
+  static constexpr int kTileBytes = BM * D * 2;       // Q tile, K tile, V tile (bf16)
+  static constexpr int kPBytes = BM * BN * 2;         // P tile (bf16)
+  static constexpr int kQ = 0;
+  static constexpr int kKV = kQ + NH * kTileBytes;
+  static constexpr int kP = kKV + STAGES * kTileBytes;
+  static constexpr int kBar = kP + NH * kPBytes;
+  // barriers: q[NH], kv_full[STAGES], kv_empty[STAGES], s_full[NH], p_full[NH], o_full[NH]
+  static constexpr int kNumBars = NH + 2 * STAGES + 3 * NH;
+  static constexpr int kTmemSlot = kBar + 8 * kNumBars;
+  static constexpr int kBytes = kTmemSlot + 16;
+  static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-B alignment
+  static constexpr int kTmemCols = (NH * (BN + D) <= 256) ? 256 : 512;
+  static constexpr int kThreads = 128 + 128 * NH;
+};
+
+struct Args {
+  int c, j, hq, G, nqt, nhp;  // chunk size, chunk index, q heads, group size, q tiles, head packs
+  float scale_log2;           // sigma * log2(e)
+  int64_t qh, qr;             // o strides (elements)
+};
+}  // namespace fwd
+
+template <int NH, int D, int STAGES>
+__global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
+    seco_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
+                          float* __restrict__ lse, const fwd::Args a) {
+  using L = fwd::Layout<NH, D, STAGES>;
+  constexpr int HALVES = D / 64;       // 64-element (128 B) swizzle boxes per row
+  constexpr int BOX = 128 * 128;       // bytes of one [128 rows][128 B] box
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sQ = sbase + L::kQ, sKV = sbase + L::kKV, sP = sbase + L::kP;
+  const uint32_t bar0 = sbase + L::kBar;
+  auto bar_q = [&](int b) { return bar0 + 8u * b; };
+  auto bar_kv_full = [&](int s) { return bar0 + 8u * (NH + s); };
+  auto bar_kv_empty = [&](int s) { return bar0 + 8u * (NH + STAGES + s); };
+  auto bar_s_full = [&](int b) { return bar0 + 8u * (NH + 2 * STAGES + b); };
+  auto bar_p_full = [&](int b) { return bar0 + 8u * (2 * NH + 2 * STAGES + b); };
+  auto bar_o_full = [&](int b) { return bar0 + 8u * (3 * NH + 2 * STAGES + b); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // heavier query tiles first (longest-processing-time order)
+  const int qt = a.nqt - 1 - (int)blockIdx.x / a.nhp;
+  const int hp = (int)blockIdx.x % a.nhp;
+  const int h0 = hp * NH, g = h0 / a.G;
+  const int q0 = a.j * a.c + qt * fwd::BM;  // absolute position of the tile's first row
+  const int T = q0 / fwd::BN + 1;           // K/V tiles 0..T-1; tile T-1 is the causal diagonal
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NH; ++b) mbar_init(bar_q(b), 1);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(bar_kv_full(s), 1); mbar_init(bar_kv_empty(s), 1); }
+    for (int b = 0; b < NH; ++b) {
+      mbar_init(bar_s_full(b), 1);
+      mbar_init(bar_p_full(b), 128);
+      mbar_init(bar_o_full(b), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tm_q); tma_prefetch(&tm_k); tma_prefetch(&tm_v); }
+  if (warp == 2) tmem_alloc<L::kTmemCols>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      for (int b = 0; b < NH; ++b) {
+        mbar_expect_tx(bar_q(b), L::kTileBytes);
+        for (int x = 0; x < HALVES; ++x)
+          tma_load_3d(sQ + b * L::kTileBytes + x * BOX, &tm_q, bar_q(b), x * 64, qt * fwd::BM, h0 + b);
+      }
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < T; ++t) {
+        for (int w = 0; w < 2; ++w) {  // K_t then V_t
+          mbar_wait(bar_kv_empty(slot), phase ^ 1);
+          mbar_expect_tx(bar_kv_full(slot), L::kTileBytes);
+          const CUtensorMap* m = w == 0 ? &tm_k : &tm_v;
+          for (int x = 0; x < HALVES; ++x)
+            tma_load_3d(sKV + slot * L::kTileBytes + x * BOX, m, bar_kv_full(slot), x * 64, t * fwd::BN, g);
+          if (++slot == STAGES) { slot = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(fwd::BM, fwd::BN, 0, 0);  // Q K-major, K K-major
+      constexpr uint32_t idesc_pv = make_idesc_bf16(fwd::BM, D, 0, 1);       // P K-major, V MN-major
+      auto issue_s = [&](int b, int slot) {
+        const uint32_t qa = sQ + b * L::kTileBytes, ka = sKV + slot * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * BOX + (kk % 4) * 32;
+          mma_ss(tmem + b * fwd::BN, make_desc_sw128(qa + off, 16, 1024), make_desc_sw128(ka + off, 16, 1024),
+                 idesc_s, kk > 0);
+        }
+      };
+      auto issue_pv = [&](int b, int slot, bool acc) {
+        const uint32_t pa = sP + b * L::kPBytes, va = sKV + slot * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < fwd::BN / 16; ++kk) {
+          const uint64_t ad = make_desc_sw128(pa + (kk / 4) * BOX + (kk % 4) * 32, 16, 1024);
+          const uint64_t bd = make_desc_sw128(va + kk * 2048, BOX, 1024);
+          mma_ss(tmem + NH * fwd::BN + b * D, ad, bd, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      for (int b = 0; b < NH; ++b) mbar_wait(bar_q(b), 0);
+      int slot = 0;
+      uint32_t phase = 0;
+      // prologue: S_b(0)
+      mbar_wait(bar_kv_full(slot), phase);
+      tc_fence_after();
+      for (int b = 0; b < NH; ++b) { issue_s(b, slot); mma_commit(bar_s_full(b)); }
+      mma_commit(bar_kv_empty(slot));
+      if (++slot == STAGES) { slot = 0; phase ^= 1; }
+      for (int t = 0; t < T; ++t) {
+        const int vslot = slot;
+        mbar_wait(bar_kv_full(vslot), phase);
+        if (++slot == STAGES) { slot = 0; phase ^= 1; }
+        const int kslot = slot;
+        const bool more = t + 1 < T;
+        for (int b = 0; b < NH; ++b) {
+          mbar_wait(bar_p_full(b), t & 1);
+          tc_fence_after();
+          issue_pv(b, vslot, t > 0);
+          mma_commit(bar_o_full(b));
+          if (more) {
+            if (b == 0) { mbar_wait(bar_kv_full(kslot), phase); tc_fence_after(); }
+            issue_s(b, kslot);
+            mma_commit(bar_s_full(b));
+          }
+        }
+        mma_commit(bar_kv_empty(vslot));
+        if (more) {
+          mma_commit(bar_kv_empty(kslot));
+          if (++slot == STAGES) { slot = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int b = (warp - 4) / 4;
+    const int wq = warp % 4;                 // TMEM lane quarter this warp may access
+    const int r = wq * 32 + lane;            // row within the tile
+    const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + b * fwd::BN;
+    const uint32_t tO = tmem + lane_addr + NH * fwd::BN + b * D;
+    const uint32_t pRow = sP + b * L::kPBytes;
+    const float sl2 = a.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int t = 0; t < T; ++t) {
+      mbar_wait(bar_s_full(b), t & 1);
+      tc_fence_after();
+      const bool diag = (t == T - 1);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int cc = 0; cc < fwd::BN / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tS + cc * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float x = (diag && cc * 32 + i > r) ? -INFINITY : __uint_as_float(v[i]);
+          mx = fmaxf(mx, x);
+        }
+      }
+      const float m_new = fmaxf(m, mx * sl2);
+      const bool need = m_new > m + fwd::kRescaleThreshold;
+      const float m_use = need ? m_new : m;
+      const float alpha = need ? ex2(m - m_new) : 1.f;
+      l *= alpha;
+      if (t > 0) mbar_wait(bar_o_full(b), (t - 1) & 1);  // PV_b(t-1) done: P_b smem and O_b free
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < fwd::BN / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tS + cc * 32, v);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = ex2(__uint_as_float(v[i]) * sl2 - m_use);
+          float p1 = ex2(__uint_as_float(v[i + 1]) * sl2 - m_use);
+          if (diag && cc * 32 + i > r) p0 = 0.f;
+          if (diag && cc * 32 + i + 1 > r) p1 = 0.f;
+          l += p0 + p1;
+          pk[i / 2] = pack_bf16(p0, p1);
+        }
+        // keys cc*32 .. cc*32+31 -> box (cc/2), 16-byte chunks (cc%2)*4 .. +3 of row r
+        const uint32_t box = pRow + (cc / 2) * BOX;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_shared_v4(box + sw128_off(r, (cc % 2) * 4 + q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
+                       pk[4 * q + 3]);
+      }
+      if (t > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t v[32];
+          tmem_ld32(tO + cc * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tmem_st32(tO + cc * 32, v);
+        }
+        tmem_wait_st();
+      }
+      m = m_use;
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(bar_p_full(b));
+    }
+    mbar_wait(bar_o_full(b), (T - 1) & 1);
+    tc_fence_after();
+    // epilogue: O = acc / l (bf16), LSE = (m + log2 l) ln 2
+    const int h = h0 + b;
+    const float inv_l = 1.f / l;
+    __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)(qt * fwd::BM + r) * a.qr;
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t v[32];
+      tmem_ld32(tO + cc * 32, v);
+      tmem_wait_ld();
+      uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(v[8 * q + 0]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l);
+        w.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l);
+        w.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l);
+        w.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l);
+        dst[q] = w;
+      }
+    }
+    lse[(int64_t)h * a.c + qt * fwd::BM + r] = (m + __log2f(l)) * 0.69314718055994531f;
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<L::kTmemCols>(tmem);
+}
+
+template <int NH, int D, int STAGES>
+static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
+                                   const CUtensorMap& tv, void* o, float* lse, cudaStream_t st) {
+  using L = fwd::Layout<NH, D, STAGES>;
+  static_assert(L::kAlloc <= 232448, "shared memory budget");
+  auto kern = seco_fwd_sm100_kernel<NH, D, STAGES>;
+  static bool attr_set = false;  // idempotent; racing setters write the same value
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  fwd::Args a;
+  a.c = g.c; a.j = g.j; a.hq = g.hq; a.G = g.hq / g.hkv;
+  a.nqt = g.c / fwd::BM; a.nhp = g.hq / NH;
+  a.scale_log2 = g.scale * 1.4426950408889634f;
+  a.qh = g.qh; a.qr = g.qr;
+  dim3 grid(a.nqt * a.nhp);
+  kern<<<grid, L::kThreads, L::kAlloc, st>>>(tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, void* o, float* lse, cudaStream_t st) {
+  const int G = g.hq / g.hkv;
+  if (g.d == 128) {
+    if (G % 2 == 0) return launch_fwd_impl<2, 128, 3>(g, tq, tk, tv, o, lse, st);
+    return launch_fwd_impl<1, 128, 4>(g, tq, tk, tv, o, lse, st);
+  }
+  if (g.d == 64) {
+    if (G % 2 == 0) return launch_fwd_impl<2, 64, 4>(g, tq, tk, tv, o, lse, st);
+    return launch_fwd_impl<1, 64, 4>(g, tq, tk, tv, o, lse, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace seco

@@ -1,0 +1,34 @@
+// Internal launcher interface between the C-ABI host layer (seco_api.cpp) and the
+// CUDA kernels.  Not part of the public ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace seco {
+
+struct ChunkGeom {
+  int hq, hkv, d, c, k, j;   // heads, head dim, chunk size, #chunks, chunk index
+  float scale;               // softmax scale sigma
+  int64_t qh, qr;            // q/o/do/dq strides (elements)
+  int64_t kh, kr;            // k/v cache strides (elements)
+};
+
+// ---- fp32 debug path (SIMT FFMA, any d <= 256, any c) -------------------------------
+cudaError_t launch_fwd_fp32(const ChunkGeom& g, const float* q, const float* k, const float* v, float* o,
+                            float* lse, cudaStream_t st);
+cudaError_t launch_bwd_fp32(const ChunkGeom& g, const float* q, const float* k, const float* v,
+                            const float* o, const float* d_o, const float* lse, float relay, float gscale,
+                            float* dkv, float* dq, float* dk_own, float* dv_own, float* ws_D,
+                            cudaStream_t st, int* launches);
+
+// ---- bf16 tensor-core path (tcgen05 / TMEM / TMA) -----------------------------------
+cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, void* o, float* lse, cudaStream_t st);
+cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tdo,
+                             const CUtensorMap& tk, const CUtensorMap& tv, const void* o, const void* d_o,
+                             const float* lse, float relay, float gscale, float* dkv, void* dq,
+                             void* dk_own, void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st,
+                             int* launches);
+
+}  // namespace seco

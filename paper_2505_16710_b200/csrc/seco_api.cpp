@@ -1,0 +1,246 @@
+// C-ABI host layer of libseco.so (see include/seco.h for the contract).
+// Validates arguments, encodes TMA tensor maps, picks the kernel variant and
+// enqueues it on the caller's stream.  Also the host SpaCO sampler.
+#include "seco.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int32_t g_launches = 0;
+
+seco_status fail(seco_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+seco_status fail(seco_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+seco_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(SECO_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+// ---- cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+  static std::once_flag once;
+  static EncodeFn fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 tensor map over [heads][rows][d], box {64, box_rows, 1}, 128-B swizzle
+bool encode_3d(CUtensorMap* m, const void* ptr, int d, int rows, int heads, int64_t row_stride,
+               int64_t head_stride, int box_rows) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)row_stride * 2, (cuuint64_t)head_stride * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+seco_status check_shape(const seco_shape* s, int32_t j) {
+  if (!s) return fail(SECO_ERR_ARG, "shape is NULL");
+  if (s->hq <= 0 || s->hkv <= 0 || s->d <= 0 || s->chunk <= 0 || s->num_chunks <= 0)
+    return fail(SECO_ERR_ARG, "non-positive size (hq=%d hkv=%d d=%d c=%d k=%d)", s->hq, s->hkv, s->d, s->chunk,
+                s->num_chunks);
+  if (s->hq % s->hkv) return fail(SECO_ERR_ARG, "hq %% hkv != 0 (hq=%d hkv=%d)", s->hq, s->hkv);
+  if (j < 0 || j >= s->num_chunks) return fail(SECO_ERR_ARG, "chunk index j=%d out of [0,%d)", j, s->num_chunks);
+  if (s->q_row_stride < s->d || s->kv_row_stride < s->d || s->q_head_stride < (int64_t)s->chunk * s->q_row_stride ||
+      s->kv_head_stride < (int64_t)s->chunk * s->num_chunks * s->kv_row_stride)
+    return fail(SECO_ERR_ARG, "strides overlap rows/heads");
+  if (s->dtype == SECO_BF16) {
+    if (s->d != 128) return fail(SECO_ERR_UNSUPPORTED, "bf16 path implements d=128 (got %d)", s->d);
+    if (s->chunk % 128) return fail(SECO_ERR_UNSUPPORTED, "bf16 path needs chunk %% 128 == 0 (got %d)", s->chunk);
+    if ((s->q_row_stride * 2) % 16 || (s->q_head_stride * 2) % 16 || (s->kv_row_stride * 2) % 16 ||
+        (s->kv_head_stride * 2) % 16)
+      return fail(SECO_ERR_ARG, "bf16 strides must be multiples of 16 bytes");
+  } else if (s->dtype == SECO_FP32_DEBUG) {
+    if (s->d > 256 || s->d % 4) return fail(SECO_ERR_UNSUPPORTED, "fp32 debug path needs d <= 256, d %% 4 == 0");
+  } else {
+    return fail(SECO_ERR_ARG, "unknown dtype %d", (int)s->dtype);
+  }
+  return SECO_OK;
+}
+
+seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
+  seco::ChunkGeom g;
+  g.hq = s->hq; g.hkv = s->hkv; g.d = s->d; g.c = s->chunk; g.k = s->num_chunks; g.j = j;
+  g.scale = s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt((float)s->d);
+  g.qh = s->q_head_stride; g.qr = s->q_row_stride; g.kh = s->kv_head_stride; g.kr = s->kv_row_stride;
+  return g;
+}
+
+size_t ws_floats(const seco_shape* s) {
+  return (size_t)s->hq * s->chunk * s->d + (size_t)s->hq * s->chunk;
+}
+
+// ---- splitmix64 (Steele, Lea & Flood 2014), state = seed
+struct SplitMix64 {
+  uint64_t x;
+  uint64_t next() {
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+};
+inline uint64_t mulhi64(uint64_t a, uint64_t b) { return (uint64_t)(((unsigned __int128)a * b) >> 64); }
+
+}  // namespace
+
+extern "C" {
+
+const char* seco_status_string(seco_status s) {
+  switch (s) {
+    case SECO_OK: return "SECO_OK";
+    case SECO_ERR_ARG: return "SECO_ERR_ARG";
+    case SECO_ERR_UNSUPPORTED: return "SECO_ERR_UNSUPPORTED";
+    case SECO_ERR_CUDA: return "SECO_ERR_CUDA";
+  }
+  return "SECO_UNKNOWN_STATUS";
+}
+
+const char* seco_last_error(void) { return g_err; }
+int32_t seco_last_launch_count(void) { return g_launches; }
+
+size_t seco_workspace_size(const seco_shape* s) {
+  if (!s || s->hq <= 0 || s->chunk <= 0 || s->d <= 0) return 0;
+  return (ws_floats(s) * 4 + 255) & ~(size_t)255;
+}
+
+seco_status seco_chunk_forward(const seco_shape* s, int32_t j, const void* q, const void* k, const void* v, void* o,
+                               float* lse, void* ws, size_t ws_bytes, seco_stream_t stream) {
+  (void)ws; (void)ws_bytes;
+  g_launches = 0;
+  seco_status st = check_shape(s, j);
+  if (st != SECO_OK) return st;
+  if (!q || !k || !v || !o || !lse) return fail(SECO_ERR_ARG, "NULL tensor pointer");
+  const seco::ChunkGeom g = geom(s, j);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (s->dtype == SECO_FP32_DEBUG) {
+    e = seco::launch_fwd_fp32(g, (const float*)q, (const float*)k, (const float*)v, (float*)o, lse, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "fwd_fp32");
+    g_launches = 1;
+    return SECO_OK;
+  }
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(SECO_ERR_ARG, "bf16 tensors must be 16-byte aligned");
+  const int S_used = (j + 1) * s->chunk;
+  CUtensorMap tq, tk, tv;
+  if (!encode_3d(&tq, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 128) ||
+      !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
+      !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128))
+    return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  e = seco::launch_fwd_sm100(g, tq, tk, tv, o, lse, cs);
+  if (e != cudaSuccess) return cuda_fail(e, "fwd_sm100");
+  g_launches = 1;
+  return SECO_OK;
+}
+
+seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, const void* k, const void* v,
+                                const void* o, const void* d_o, const float* lse, float relay_scale,
+                                float grad_scale, float* dkv, void* dq, void* dk_own, void* dv_own, void* ws,
+                                size_t ws_bytes, seco_stream_t stream) {
+  g_launches = 0;
+  seco_status st = check_shape(s, j);
+  if (st != SECO_OK) return st;
+  if (!q || !k || !v || !o || !d_o || !lse || !dkv || !dq) return fail(SECO_ERR_ARG, "NULL tensor pointer");
+  if (!ws || ws_bytes < seco_workspace_size(s)) return fail(SECO_ERR_ARG, "workspace too small");
+  if (!aligned16(dkv) || !aligned16(ws)) return fail(SECO_ERR_ARG, "dkv / ws must be 16-byte aligned");
+  if (!std::isfinite(relay_scale) || !std::isfinite(grad_scale)) return fail(SECO_ERR_ARG, "non-finite scale");
+  const seco::ChunkGeom g = geom(s, j);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  float* wsf = reinterpret_cast<float*>(ws);
+  float* ws_dqacc = wsf;
+  float* ws_D = wsf + (size_t)s->hq * s->chunk * s->d;
+  int launches = 0;
+  cudaError_t e;
+  if (s->dtype == SECO_FP32_DEBUG) {
+    e = seco::launch_bwd_fp32(g, (const float*)q, (const float*)k, (const float*)v, (const float*)o,
+                              (const float*)d_o, lse, relay_scale, grad_scale, dkv, (float*)dq, (float*)dk_own,
+                              (float*)dv_own, ws_D, cs, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "bwd_fp32");
+    g_launches = launches;
+    return SECO_OK;
+  }
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(d_o) || !aligned16(dq))
+    return fail(SECO_ERR_ARG, "bf16 tensors must be 16-byte aligned");
+  const int S_used = (j + 1) * s->chunk;
+  CUtensorMap tq, tdo, tk, tv;
+  if (!encode_3d(&tq, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64) ||
+      !encode_3d(&tdo, d_o, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64) ||
+      !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
+      !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128))
+    return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  e = seco::launch_bwd_sm100(g, tq, tdo, tk, tv, o, d_o, lse, relay_scale, grad_scale, dkv, dq, dk_own, dv_own,
+                             ws_dqacc, ws_D, cs, &launches);
+  if (e != cudaSuccess) return cuda_fail(e, "bwd_sm100");
+  g_launches = launches;
+  return SECO_OK;
+}
+
+seco_status spaco_sample_and_scale(int32_t k, int32_t t, uint64_t seed, float cap, spaco_mode mode,
+                                   int32_t* idx_out, int32_t* n_out, float* relay_scale_out,
+                                   float* seed_scale_out) {
+  if (!idx_out || !n_out || !relay_scale_out || !seed_scale_out) return fail(SECO_ERR_ARG, "NULL output");
+  if (k < 1 || t < 1 || t > k) return fail(SECO_ERR_ARG, "need 1 <= t <= k (k=%d t=%d)", k, t);
+  if (mode == SPACO_HT && t < 2) return fail(SECO_ERR_ARG, "SPACO_HT needs t >= 2");
+  if (mode != SPACO_PAPER && mode != SPACO_HT && mode != SPACO_BERNOULLI)
+    return fail(SECO_ERR_ARG, "unknown mode %d", (int)mode);
+  SplitMix64 rng{seed};
+  int32_t n = 0;
+  if (mode == SPACO_BERNOULLI) {
+    for (int32_t i = 0; i < k; ++i)
+      if (mulhi64(rng.next(), (uint64_t)k) < (uint64_t)t) idx_out[n++] = i;
+  } else {
+    // partial Fisher-Yates over a = [0..k-1] held in idx_out
+    for (int32_t i = 0; i < k; ++i) idx_out[i] = i;
+    for (int32_t r = 0; r < t; ++r) {
+      const int32_t jj = r + (int32_t)mulhi64(rng.next(), (uint64_t)(k - r));
+      std::swap(idx_out[r], idx_out[jj]);
+    }
+    n = t;
+  }
+  std::sort(idx_out, idx_out + n, [](int32_t a, int32_t b) { return a > b; });
+  double gamma, sscale;
+  if (mode == SPACO_PAPER) { gamma = (double)k / t; sscale = 1.0; }
+  else if (mode == SPACO_HT) { gamma = (double)(k - 1) / (t - 1); sscale = (double)k / t; }
+  else { gamma = (double)k / t; sscale = (double)k / t; }
+  float g32 = (float)gamma;
+  if (cap > 0.f) g32 = std::min(g32, cap);
+  *relay_scale_out = g32;
+  *seed_scale_out = (float)sscale;
+  *n_out = n;
+  return SECO_OK;
+}
+
+}  // extern "C"

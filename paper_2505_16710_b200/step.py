@@ -1,0 +1,115 @@
+"""SeCO / SpaCO step driver for one attention layer (Alg. 1, Alg. 2
+P:319-338).  Owns the persistent device buffers of a step (outputs O / LSE, the
+fp32 checkpoint-gradient buffer dKV, dQ, workspace) and issues the chunk calls
+in the algorithm's order on one CUDA stream.  Torch is used for memory and
+streams only; all arithmetic is in libseco.so."""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import ops
+from .flops import seco_step_flops, spaco_step_flops
+
+
+@dataclass
+class StepResult:
+    selected: list = field(default_factory=list)   # chunk indices processed in stage 2 (descending)
+    relay_scale: float = 1.0
+    seed_scale: float = 1.0
+    flops: float = 0.0                               # algorithmic FLOPs of the step (flops.py)
+    launches: int = 0                                # kernels enqueued by libseco.so
+
+
+class ChunkedAttention:
+    """Buffers + call sequence for one causal GQA attention layer over a sequence
+    of k chunks.  dkv[0] / dkv[1] hold, after a step, the gradient of every
+    chunk's own K / V (slot j = total own-chunk gradient after chunk j's relay)."""
+
+    def __init__(self, hq, hkv, d, seq, chunk, dtype=torch.bfloat16, device="cuda", softmax_scale=0.0,
+                 own_copies=False):
+        if seq % chunk:
+            raise ValueError("seq must be a multiple of chunk")
+        self.hq, self.hkv, self.d, self.seq, self.chunk = hq, hkv, d, seq, chunk
+        self.k = seq // chunk
+        self.dtype, self.device = dtype, torch.device(device)
+        dev = self.device
+        self.o = torch.empty(hq, seq, d, dtype=dtype, device=dev)
+        self.lse = torch.empty(self.k, hq, chunk, dtype=torch.float32, device=dev)   # LSE_j dense [hq][c]
+        self.dq = torch.empty(hq, seq, d, dtype=dtype, device=dev)
+        self.dkv = torch.empty(2, hkv, seq, d, dtype=torch.float32, device=dev)
+        self.own = torch.empty(2, hkv, chunk, d, dtype=dtype, device=dev) if own_copies else None
+        probe_q = torch.empty(hq, seq, d, dtype=dtype, device="meta")
+        probe_k = torch.empty(hkv, seq, d, dtype=dtype, device="meta")
+        self.shape = ops.make_shape(probe_q, probe_k, chunk, softmax_scale)
+        self.ws = torch.empty(max(ops.seco_workspace_size(self.shape) // 4, 1), dtype=torch.float32, device=dev)
+
+    # ---- per-chunk calls -------------------------------------------------------------
+    def _lse(self, j):
+        return self.lse[j]
+
+    def lse_full(self):
+        """LSE as [hq][S] (a copy)."""
+        return self.lse.permute(1, 0, 2).reshape(self.hq, self.seq)
+
+    def forward_chunk(self, q, k_cache, v_cache, j, stream=None):
+        ops.seco_chunk_forward(self.shape, j, ops.chunk_view(q, self.shape, j), k_cache, v_cache,
+                               ops.chunk_view(self.o, self.shape, j), self._lse(j), self.ws, stream)
+        return ops.last_launch_count()
+
+    def backward_chunk(self, q, k_cache, v_cache, do, j, relay_scale=1.0, grad_scale=1.0, stream=None):
+        dk_own = self.own[0] if self.own is not None else None
+        dv_own = self.own[1] if self.own is not None else None
+        ops.seco_chunk_backward(self.shape, j, ops.chunk_view(q, self.shape, j), k_cache, v_cache,
+                                ops.chunk_view(self.o, self.shape, j), ops.chunk_view(do, self.shape, j),
+                                self._lse(j), relay_scale, grad_scale, self.dkv,
+                                ops.chunk_view(self.dq, self.shape, j), dk_own, dv_own, self.ws, stream)
+        return ops.last_launch_count()
+
+    # ---- whole steps ---------------------------------------------------------------
+    def _check(self, q, k_cache, v_cache, do):
+        for t, h in ((q, self.hq), (do, self.hq), (k_cache, self.hkv), (v_cache, self.hkv)):
+            if t.shape != (h, self.seq, self.d) or t.dtype != self.dtype or t.device != self.device:
+                raise ValueError("input tensor shape / dtype / device mismatch")
+            if not t.is_contiguous():
+                raise ValueError("inputs must be contiguous [heads][seq][d]")
+
+    def step(self, q, k_cache, v_cache, do, selected=None, relay_scale=1.0, grad_scale=1.0, stream=None):
+        """Stage 1: forward of every chunk, ascending (Alg. 1/2 lines 1-3).
+        Stage 2: for j in `selected` (default: all) descending -- rebuild (forward)
+        then backward with relay (Alg. 1 lines 4-7; Alg. 2 lines 5-8)."""
+        self._check(q, k_cache, v_cache, do)
+        sel = list(range(self.k)) if selected is None else sorted(set(int(i) for i in selected))
+        sel = sel[::-1]
+        self.dkv.zero_()          # checkpoint grads m'.grad start at zero each step (caller-owned buffer)
+        if selected is not None:
+            self.dq.zero_()       # rows of non-selected chunks keep dQ = 0 (reading Z11)
+        launches = 0
+        for j in range(self.k):
+            launches += self.forward_chunk(q, k_cache, v_cache, j, stream)
+        for j in sel:
+            launches += self.forward_chunk(q, k_cache, v_cache, j, stream)
+            launches += self.backward_chunk(q, k_cache, v_cache, do, j, relay_scale, grad_scale, stream)
+        if selected is None:
+            fl = seco_step_flops(self.hq, self.d, self.seq, self.chunk)
+        else:
+            fl = spaco_step_flops(self.hq, self.d, self.seq, self.chunk, sel)
+        return StepResult(sel, relay_scale, grad_scale, fl, launches)
+
+    def seco_step(self, q, k_cache, v_cache, do, stream=None):
+        return self.step(q, k_cache, v_cache, do, None, 1.0, 1.0, stream)
+
+    def spaco_step(self, q, k_cache, v_cache, do, t, seed, cap=2.0, mode=ops._lib.SPACO_PAPER, stream=None):
+        idx, gamma, s = ops.spaco_sample_and_scale(self.k, t, seed, cap, mode)
+        r = self.step(q, k_cache, v_cache, do, idx, gamma, s, stream)
+        r.selected, r.relay_scale, r.seed_scale = idx, gamma, s
+        return r
+
+    @property
+    def dk(self):
+        return self.dkv[0]
+
+    @property
+    def dv(self):
+        return self.dkv[1]

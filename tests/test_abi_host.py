@@ -1,0 +1,137 @@
+"""CPU-side checks of the C ABI (no GPU needed): libseco.so loads and exports every
+symbol include/seco.h declares; the host sampler agrees bit for bit with the
+oracle's independent implementation; argument validation rejects bad calls
+before any CUDA work; FLOP accounting matches brute-force pair counting."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import sampler as OS
+from paper_2505_16710_b200 import _lib, flops
+from paper_2505_16710_b200.build import build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build()
+    return _lib.load()
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "seco.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(seco_\w+|spaco_\w+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    declared = _declared_functions()
+    assert set(declared) == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_status_strings(lib):
+    for code, name in enumerate(["SECO_OK", "SECO_ERR_ARG", "SECO_ERR_UNSUPPORTED", "SECO_ERR_CUDA"]):
+        assert lib.seco_status_string(code).decode() == name
+
+
+def _c_sample(k, t, seed, cap, mode):
+    from paper_2505_16710_b200 import ops
+    return ops.spaco_sample_and_scale(k, t, seed, cap, mode)
+
+
+@pytest.mark.parametrize("mode", [_lib.SPACO_PAPER, _lib.SPACO_HT, _lib.SPACO_BERNOULLI])
+def test_sampler_bit_exact_vs_oracle(lib, mode):
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        k = int(rng.integers(2, 70))
+        t = int(rng.integers(2 if mode == _lib.SPACO_HT else 1, k + 1))
+        seed = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
+        cap = float(rng.choice([0.0, 2.0, 1.5]))
+        idx, g, s = _c_sample(k, t, seed, cap, mode)
+        oidx, og, os_ = OS.sample_and_scale(k, t, seed, cap, mode)
+        assert idx == oidx
+        assert np.float32(g) == np.float32(og) and np.float32(s) == np.float32(os_)
+
+
+def test_sampler_kats_golden(lib):
+    path = os.path.join(ROOT, "tests", "golden", "sampler_kats.txt")
+    for ln in open(path):
+        if not ln.strip() or ln.startswith("#"):
+            continue
+        mode, k, t, seed, want = ln.split()
+        m = _lib.SPACO_PAPER if mode == "T_OF_K" else _lib.SPACO_BERNOULLI
+        idx, _, _ = _c_sample(int(k), int(t), int(seed), 0.0, m)
+        assert idx == [int(x) for x in want.split(",")]
+
+
+def test_sampler_errors(lib):
+    from paper_2505_16710_b200 import ops
+    for k, t, mode in ((4, 0, 0), (4, 5, 0), (4, 1, _lib.SPACO_HT), (0, 0, 0), (4, 2, 7)):
+        with pytest.raises(_lib.SecoError):
+            ops.spaco_sample_and_scale(k, t, 0, 2.0, mode)
+
+
+def _shape(**kw):
+    d = dict(hq=32, hkv=8, d=128, chunk=256, num_chunks=4, softmax_scale=0.0, dtype=0,
+             q_head_stride=1024 * 128, q_row_stride=128, kv_head_stride=1024 * 128, kv_row_stride=128)
+    d.update(kw)
+    return _lib.SecoShape(*[d[f] for f, _ in _lib.SecoShape._fields_])
+
+
+@pytest.mark.parametrize("kw,j,code", [
+    (dict(), -1, _lib.SECO_ERR_ARG),
+    (dict(), 4, _lib.SECO_ERR_ARG),
+    (dict(hkv=5), 0, _lib.SECO_ERR_ARG),
+    (dict(d=96, q_row_stride=96, kv_row_stride=96), 0, _lib.SECO_ERR_UNSUPPORTED),
+    (dict(chunk=192, q_head_stride=768 * 128, kv_head_stride=768 * 128), 0, _lib.SECO_ERR_UNSUPPORTED),
+    (dict(q_row_stride=100), 0, _lib.SECO_ERR_ARG),
+    (dict(dtype=1, d=300, q_row_stride=300, kv_row_stride=300, q_head_stride=1024 * 300,
+          kv_head_stride=1024 * 300), 0, _lib.SECO_ERR_UNSUPPORTED),
+    (dict(dtype=5), 0, _lib.SECO_ERR_ARG),
+])
+def test_argument_validation(lib, kw, j, code):
+    s = _shape(**kw)
+    dummy = ctypes.c_void_p(1 << 20)  # never dereferenced: validation happens before any launch
+    r = lib.seco_chunk_forward(ctypes.byref(s), j, dummy, dummy, dummy, dummy, dummy, None, 0, None)
+    assert r == code, lib.seco_last_error()
+    r = lib.seco_chunk_backward(ctypes.byref(s), j, dummy, dummy, dummy, dummy, dummy, dummy, 1.0, 1.0,
+                                dummy, dummy, None, None, dummy, 1 << 30, None)
+    assert r == code, lib.seco_last_error()
+
+
+def test_null_pointers_rejected(lib):
+    s = _shape()
+    r = lib.seco_chunk_forward(ctypes.byref(s), 0, None, None, None, None, None, None, 0, None)
+    assert r == _lib.SECO_ERR_ARG
+    dummy = ctypes.c_void_p(1 << 20)
+    r = lib.seco_chunk_backward(ctypes.byref(s), 0, dummy, dummy, dummy, dummy, dummy, dummy, 1.0, 1.0,
+                                dummy, dummy, None, None, dummy, 16, None)   # workspace too small
+    assert r == _lib.SECO_ERR_ARG
+
+
+def test_workspace_size(lib):
+    s = _shape()
+    assert lib.seco_workspace_size(ctypes.byref(s)) >= 4 * (32 * 256 * 128 + 32 * 256)
+
+
+def test_flops_pairs_brute_force():
+    for c, k in ((16, 4), (7, 5), (128, 3)):
+        S = c * k
+        tot = 0
+        for j in range(k):
+            brute = sum(1 for p in range(j * c, (j + 1) * c) for q in range(S) if q <= p)
+            assert flops.pairs(c, j) == brute
+            tot += brute
+        assert tot == S * (S + 1) // 2
+    # SeCO = 4.5 F ; SpaCO with all chunks = SeCO
+    hq, d, S, c = 32, 128, 32768, 2048
+    F = flops.total_fwd(hq, d, S)
+    assert abs(flops.seco_step_flops(hq, d, S, c) / F - 4.5) < 1e-12
+    assert abs(F - 8.796e12) / 8.796e12 < 1e-3     # cfg3 F = 8.796 TF
+    assert flops.spaco_step_flops(hq, d, S, c, range(16)) == flops.seco_step_flops(hq, d, S, c)
