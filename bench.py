@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the SeCO / SpaCO chunked-attention hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--mode seco|spaco]
+                    [--t 4] [--shard heads|batch] [--impl ours|reference]
+
+One step = one pass of the whole hot path over one sequence:
+stage 1 (chunk forward, j = 0..k-1) then stage 2 (for j = k-1..0 in the sampled set:
+rebuild forward + chunk backward with relay), all through the C ABI of libseco.so on
+one CUDA stream.  Metric (BASELINE.json): algorithmic TFLOP/s of the step (SeCO =
+4.5 F, F = 2 d Hq S (S+1); SpaCO = F + 3.5 sum_{j in I} fwd_j), plus tokens/s.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): `--shard heads` gives rank r the
+kv-head group slice [r Hkv/N, (r+1) Hkv/N) and the matching q heads (no collective
+on the attention path; total work fixed -> "strong"); `--shard batch` gives every
+rank its own sequence ("weak").  Time = max over ranks of the CUDA-event time.
+
+`--impl reference` times the CPU oracle (oracle/, fp64 NumPy) on the host cores on a
+bounded sample of the same workload (the reference arm; rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "chunked attn fwd+bwd TFLOP/s & tokens/s, Llama-3-8B shape, 32K ctx"
+CONFIGS = {
+    # BASELINE.json configs[1..4]; configs[0] (tiny) is a parity case only
+    "cfg2": dict(hq=32, hkv=8, d=128, seq=8192, chunk=1024),
+    "cfg3": dict(hq=32, hkv=8, d=128, seq=32768, chunk=2048),
+    "cfg4": dict(hq=32, hkv=8, d=128, seq=131072, chunk=4096),
+    "cfg5": dict(hq=32, hkv=8, d=128, seq=16384, chunk=1024),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="seco", choices=["seco", "spaco"])
+    ap.add_argument("--t", type=int, default=4, help="SpaCO budget (sampled chunks)")
+    ap.add_argument("--cap", type=float, default=2.0)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--shard", default="heads", choices=["heads", "batch"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no timing output")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while the timed region runs."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_sample(cfg, steps=1):
+    """Time the oracle (fp64 NumPy, as it stands) on a bounded sample of the workload:
+    a SeCO step over the first 2 chunks of the sequence for ONE q-head / ONE kv-head.
+    Returns (TFLOP/s, seconds per sample, description, threads)."""
+    import numpy as np
+    from oracle import chunkwise as OC
+    from synth import make_inputs
+    from paper_2505_16710_b200.flops import seco_step_flops
+    c, d = cfg["chunk"], cfg["d"]
+    seq = 2 * c
+    x = make_inputs(1, 1, seq, d, seed=0)
+    fl = seco_step_flops(1, d, seq, c)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        OC.seco_step(x.q, x.k, x.v, x.do, [c, c])
+        times.append(time.perf_counter() - t0)
+    dt = min(times) if steps > 1 else times[0]
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    desc = (f"oracle.chunkwise.seco_step fp64 on 1 q-head x 1 kv-head, first {seq} tokens "
+            f"(2 chunks of {c}), d={d}: {fl / 1e9:.1f} GFLOP algorithmic")
+    return fl / dt / 1e12, dt, desc, threads
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    for _ in range(args.warmup):
+        cpu_oracle_sample(cfg, 1)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        v, dt, desc, threads = cpu_oracle_sample(cfg, 1)
+        vals.append(v)
+        t_all += dt
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+            "higher_is_better": True, "scaling": "strong" if (args.shard == "heads" and world > 1) else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} SeCO, bounded host sample", **cfg},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from synth import make_inputs
+    from paper_2505_16710_b200.step import ChunkedAttention
+    from paper_2505_16710_b200 import ops, flops as FL
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = dict(CONFIGS[args.config])
+    hq, hkv, d, seq, c = cfg["hq"], cfg["hkv"], cfg["d"], cfg["seq"], cfg["chunk"]
+    if args.shard == "heads" and world > 1:
+        if hkv % world:
+            raise SystemExit(f"--shard heads needs Hkv % N == 0 (Hkv={hkv}, N={world})")
+        hq_r, hkv_r = hq // world, hkv // world
+    else:
+        hq_r, hkv_r = hq, hkv
+    k = seq // c
+
+    # inputs: seeded on the host (synth), pinned, then resident in HBM for the device timing
+    x = make_inputs(hq_r, hkv_r, seq, d, seed=args.seed + 1000 * rank)
+    pinned = []
+    for bits in (x.q_bits, x.k_bits, x.v_bits, x.do_bits):
+        t = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).pin_memory()
+        pinned.append(t)
+    del x
+    q, kc, vc, do = (t.to(dev, non_blocking=True) for t in pinned)
+    layer = ChunkedAttention(hq_r, hkv_r, d, seq, c, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def sampled():
+        if args.mode == "seco":
+            return None, 1.0, 1.0
+        return ops.spaco_sample_and_scale(k, args.t, args.seed, args.cap, ops._lib.SPACO_PAPER)
+
+    sel, gamma, sscale = sampled()
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            layer.step(q, kc, vc, do, sel, gamma, sscale)
+        torch.cuda.synchronize()
+        return
+
+    # ---------------------------------------------------------------- warm-up
+    for _ in range(max(args.warmup, 0)):
+        layer.step(q, kc, vc, do, sel, gamma, sscale)
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed (device-resident inputs)
+    # per-call CUDA events on the launching stream, to attribute time to the fwd / bwd kernels
+    order = [("f", j) for j in range(k)]
+    stage2 = list(range(k))[::-1] if sel is None else sorted(sel, reverse=True)
+    for j in stage2:
+        order += [("f", j), ("b", j)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(order))] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    clk = ClockSampler(local_rank)
+    with clk:
+        t_start.record(stream)
+        for s in range(args.steps):
+            layer.dkv.zero_()
+            if sel is not None:
+                layer.dq.zero_()
+            for n, (kind, j) in enumerate(order):
+                ev[s][2 * n].record(stream)
+                if kind == "f":
+                    launches += layer.forward_chunk(q, kc, vc, j)
+                else:
+                    launches += layer.backward_chunk(q, kc, vc, do, j, gamma, sscale)
+                ev[s][2 * n + 1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_local = t_start.elapsed_time(t_end)
+    t_f = t_b = 0.0
+    for s in range(args.steps):
+        for n, (kind, j) in enumerate(order):
+            dt = ev[s][2 * n].elapsed_time(ev[s][2 * n + 1])
+            if kind == "f":
+                t_f += dt
+            else:
+                t_b += dt
+    ms = ms_local
+    if world > 1:
+        tt = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+
+    step_flops_rank = FL.seco_step_flops(hq_r, d, seq, c) if sel is None else \
+        FL.spaco_step_flops(hq_r, d, seq, c, sel)
+    n_seq = world if (args.shard == "batch" or world == 1) else 1
+    total_flops = step_flops_rank * world          # all ranks' work per step
+    tokens = seq * n_seq
+    value = total_flops / (ms_per_step * 1e-3) / 1e12
+    # dominant kernel: algorithmic flops per launch / average launch time (this rank)
+    fwd_fl = sum(FL.fwd_flops(hq_r, d, c, j) for kind, j in order if kind == "f") * args.steps
+    bwd_fl = sum(FL.bwd_flops(hq_r, d, c, j) for kind, j in order if kind == "b") * args.steps
+    kern = {"fwd": {"tflops": fwd_fl / (t_f * 1e-3) / 1e12 if t_f else None, "ms_per_step": t_f / args.steps,
+                    "share_of_step": t_f / ms_local},
+            "bwd": {"tflops": bwd_fl / (t_b * 1e-3) / 1e12 if t_b else None, "ms_per_step": t_b / args.steps,
+                    "share_of_step": t_b / ms_local}}
+    dom = "bwd" if t_b >= t_f else "fwd"
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak, peak_src = peaks["bf16_tflops_sustained"], "MEASURED_PEAKS.json bf16_tflops_sustained"
+        peak_burst = peaks["bf16_tflops"]
+    except Exception:
+        peak, peak_src, peak_burst = 1400.0, "fallback B200_PROFILING.md sustained ~1.4 PF", 1590.0
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        traffic = tr.get(dom, {}).get(args.config)
+    except Exception:
+        pass
+    achieved = kern[dom]["tflops"]
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "kernel": f"seco_chunk_{'backward' if dom == 'bwd' else 'forward'} "
+                          f"({'bwd_prep + seco_bwd_sm100_kernel + bwd_final' if dom == 'bwd' else 'seco_fwd_sm100_kernel'})",
+                "peak_source": peak_src, "frac_of_burst_peak": achieved / peak_burst if achieved else None}
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        out_dq = torch.empty(layer.dq.shape, dtype=layer.dq.dtype).pin_memory()
+        out_dkv = torch.empty(layer.dkv.shape, dtype=layer.dkv.dtype).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in pinned)
+        d2h = out_dq.numel() * out_dq.element_size() + out_dkv.numel() * out_dkv.element_size()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for s in range(args.steps):
+            for dst, src in zip((q, kc, vc, do), pinned):
+                dst.copy_(src, non_blocking=True)
+            layer.step(q, kc, vc, do, sel, gamma, sscale)
+            out_dq.copy_(layer.dq, non_blocking=True)
+            out_dkv.copy_(layer.dkv, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": total_flops / (ems / args.steps * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": ems / args.steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "pinned host Q,K,V,dO -> device; SeCO/SpaCO step via C ABI; dQ, dKV -> pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, desc, threads = cpu_oracle_sample(cfg, 1)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": desc,
+               "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if (args.shard == "heads" and world > 1) else "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: Llama-3-8B attention shape, seq {seq}, chunk {c}, "
+                                   f"{args.mode}" + (f" t={args.t} of {k} (I={sel}, gamma={gamma})"
+                                                     if sel is not None else ""),
+                       "hq": hq, "hkv": hkv, "d": d, "seq_len": seq, "chunk": c, "num_chunks": k,
+                       "mode": args.mode, "sequences_per_step": n_seq,
+                       "parallelism": f"{args.shard}{world}" if world > 1 else "single",
+                       "l2_policy": "inputs larger than L2 (Q,dO 256 MiB, K,V 64 MiB each, dKV 256 MiB per rank)"},
+            "tokens_per_s": tokens / (ms_per_step * 1e-3),
+            "step_tflop": total_flops / 1e12,
+            "roofline": roofline, "kernels": kern,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

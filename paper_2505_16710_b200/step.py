@@ -33,7 +33,10 @@ class ChunkedAttention:
             raise ValueError("seq must be a multiple of chunk")
         self.hq, self.hkv, self.d, self.seq, self.chunk = hq, hkv, d, seq, chunk
         self.k = seq // chunk
-        self.dtype, self.device = dtype, torch.device(device)
+        dev = torch.device(device)
+        if dev.type == "cuda" and dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.dtype, self.device = dtype, dev
         dev = self.device
         self.o = torch.empty(hq, seq, d, dtype=dtype, device=dev)
         self.lse = torch.empty(self.k, hq, chunk, dtype=torch.float32, device=dev)   # LSE_j dense [hq][c]
