@@ -85,6 +85,7 @@ class ChunkedAttention:
         self._check(q, k_cache, v_cache, do)
         sel = list(range(self.k)) if selected is None else sorted(set(int(i) for i in selected))
         sel = sel[::-1]
+        self.last_selected = sel
         self.dkv.zero_()          # checkpoint grads m'.grad start at zero each step (caller-owned buffer)
         if selected is not None:
             self.dq.zero_()       # rows of non-selected chunks keep dQ = 0 (reading Z11)
@@ -111,8 +112,23 @@ class ChunkedAttention:
 
     @property
     def dk(self):
+        """Gradient of every chunk's own K after the last step (a view of dkv[0]).  For a
+        SpaCO step, slots of non-selected chunks still hold their never-relayed
+        checkpoint gradient; use own_grads() for the per-chunk gradients (zero there)."""
         return self.dkv[0]
 
     @property
     def dv(self):
         return self.dkv[1]
+
+    def own_grads(self):
+        """(dK, dV) of each chunk's own K/V after the last step: dkv slots of the chunks
+        processed in stage 2, zero for chunks that were not sampled (reading Z11).
+        Result extraction (a copy), not part of the hot path."""
+        dk, dv = self.dkv[0].clone(), self.dkv[1].clone()
+        sel = set(getattr(self, "last_selected", range(self.k)))
+        for j in range(self.k):
+            if j not in sel:
+                dk[:, j * self.chunk:(j + 1) * self.chunk] = 0
+                dv[:, j * self.chunk:(j + 1) * self.chunk] = 0
+        return dk, dv

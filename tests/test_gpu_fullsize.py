@@ -1,0 +1,91 @@
+"""Parity at the benchmark's full size (BASELINE configs[2] = cfg3: 32 q / 8 kv heads,
+d=128, seq 32768, chunk 2048) in the launch configuration bench.py times (the same
+ChunkedAttention step through the C ABI).  The oracle cannot afford the whole
+sequence, so it checks
+  * sampled rows one by one: O, LSE and dQ of a query row depend only on that row
+    (oracle chunk_fwd / chunk_bwd on a one-row "chunk" at its absolute position);
+  * dK, dV of keys in the last chunk: only the last chunk's rows see them
+    (oracle chunk_bwd of the last chunk for one kv-head group);
+  * properties that hold at any size: sum over keys of dK is 0 (rows of dS sum to
+    0) and sum over keys of dV equals the sum of dO over the group's rows (rows of P
+    sum to 1)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention as OA
+from oracle import sampler as OS
+from tests.gpu_util import BF16_TOL, err, host, upload
+from synth import make_inputs
+
+pytestmark = pytest.mark.gpu
+
+HQ, HKV, D, S, C = 32, 8, 128, 32768, 2048
+G = HQ // HKV
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    x = make_inputs(HQ, HKV, S, D, seed=0)
+    q, k, v, do = upload(x, torch.bfloat16)
+    from paper_2505_16710_b200.step import ChunkedAttention
+    layer = ChunkedAttention(HQ, HKV, D, S, C, dtype=torch.bfloat16)
+    return x, (q, k, v, do), layer
+
+
+ROWS = [(0, 0), (5, 2047), (13, 2048), (22, 7 * 2048 + 1000), (31, 15 * 2048 + 3), (17, S - 1), (8, 9 * 2048 + 2047)]
+
+
+def _row_ref(x, h, p):
+    g = h // G
+    qr, dor = x.q[h:h + 1, p:p + 1], x.do[h:h + 1, p:p + 1]
+    o, lse = OA.chunk_fwd(qr, x.k[g:g + 1], x.v[g:g + 1], p)
+    dq, _, _ = OA.chunk_bwd(qr, x.k[g:g + 1], x.v[g:g + 1], dor, p)
+    return o[0, 0], lse[0, 0], dq[0, 0]
+
+
+def test_cfg3_seco_sampled_rows_and_invariants(cfg3):
+    x, (q, k, v, do), layer = cfg3
+    layer.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    o_g, dq_g = host(layer.o), host(layer.dq)
+    lse_g = host(layer.lse_full())
+    o_r, l_r, dq_r, o_s, l_s, dq_s = [], [], [], [], [], []
+    for h, p in ROWS:
+        a, b, c = _row_ref(x, h, p)
+        o_r.append(a); l_r.append(b); dq_r.append(c)
+        o_s.append(o_g[h, p]); l_s.append(lse_g[h, p]); dq_s.append(dq_g[h, p])
+    assert err(np.array(o_s), np.array(o_r)) <= BF16_TOL
+    assert err(np.array(l_s), np.array(l_r)) <= BF16_TOL
+    assert err(np.array(dq_s), np.array(dq_r)) <= BF16_TOL
+    # keys of the last chunk, kv-head group 5: exact from the last chunk's rows
+    g = 5
+    a0 = S - C
+    _, dk_src, dv_src = OA.chunk_bwd(x.q[g * G:(g + 1) * G, a0:], x.k[g:g + 1], x.v[g:g + 1],
+                                     x.do[g * G:(g + 1) * G, a0:], a0)
+    dk_g = host(layer.dk[g, a0:])
+    dv_g = host(layer.dv[g, a0:])
+    assert err(dk_g, dk_src[0, a0:]) <= BF16_TOL
+    assert err(dv_g, dv_src[0, a0:]) <= BF16_TOL
+    # any-size properties over the whole sequence, every kv head
+    dk_all = layer.dk.double().sum(dim=1).cpu().numpy()                  # [hkv][d], exactly 0
+    dk_abs = layer.dk.double().abs().sum(dim=1).cpu().numpy()
+    assert np.abs(dk_all).max() <= BF16_TOL * dk_abs.max()
+    dv_sum = layer.dv.double().sum(dim=1).cpu().numpy()
+    do_sum = x.do.astype(np.float64).reshape(HKV, G, S, D).sum(axis=(1, 2))
+    assert err(dv_sum, do_sum) <= BF16_TOL
+
+
+def test_cfg3_spaco_sampled_rows(cfg3):
+    x, (q, k, v, do), layer = cfg3
+    r = layer.spaco_step(q, k, v, do, 4, 0, cap=2.0, mode=OS.PAPER)
+    torch.cuda.synchronize()
+    assert r.selected == OS.sample_indices(16, 4, 0, OS.PAPER)
+    dq_g = host(layer.dq)
+    for h, p in ROWS:
+        j = p // C
+        if j in r.selected:
+            _, _, ref = _row_ref(x, h, p)
+            assert err(dq_g[h, p], r.seed_scale * ref) <= BF16_TOL
+        else:
+            assert np.abs(dq_g[h, p]).max() == 0.0
