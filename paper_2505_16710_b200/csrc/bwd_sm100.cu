@@ -12,15 +12,17 @@
 //   P^T  = exp2(S^T sigma log2e - LSE log2e), dS^T = P^T o (dP^T - D)   (CUDA cores, -> smem bf16)
 //   dV  += P^T dO         [128 keys x d]      A K-major (smem), B MN-major
 //   dK  += dS^T Q         [128 keys x d]
-//   dQ^T = K^T dS^T       [d x 64 q]          A and B MN-major; red.add into fp32 dQacc
+//   dQ^T = K^T dS^T       [d x 64 q]          A and B MN-major; -> smem -> TMA reduce-add into fp32 dQacc
 // Warp roles: w0 TMA producer (K,V once; Q,dO,LSE,D per tile through a ring),
 // w1 MMA issuer, w2 TMEM allocator, w4-w11 two compute warpgroups (thread = key row,
 // 32 query columns each), w12-w15 dQ drain (thread = head-dim lane).
 // MMA issue order per tile i: [S^T, dP^T](i+1) -> dV(i), dK(i) -> dQ^T(i), so the
 // elementwise work of tile i+1 overlaps the tensor-core work of tile i.
 // TMEM columns: S^T [0,64) dP^T [64,128) dQ^T x2 [128,256) dK [256,384) dV [384,512).
-// dK/dV leave TMEM once per CTA, scaled (s*sigma, s), via red.add.v4.f32 into dkv
-// (slot j was pre-scaled by the relay factor gamma in bwd_prep).
+// dK/dV leave TMEM once per CTA, scaled (s*sigma, s), through 128B-swizzled smem staging and
+// TMA tensor reduce-add (cp.reduce.async.bulk.tensor ... .add) into dkv (slot j was pre-scaled
+// by the relay factor gamma in bwd_prep).  All fp32 reductions run in L2, issued by the TMA
+// unit, so no thread issues per-element atomics.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -45,7 +47,9 @@ constexpr int kQ = kV + kKVBytes;                       // [STAGES] Q tiles
 constexpr int kDO = kQ + STAGES * kQBytes;              // [STAGES] dO tiles
 constexpr int kP = kDO + STAGES * kQBytes;              // [2] P^T
 constexpr int kDS = kP + 2 * kPBytes;                   // [2] dS^T
-constexpr int kStats = kDS + 2 * kPBytes;               // [STAGES][2][BQ] fp32 (LSE, D)
+constexpr int kDQ = kDS + 2 * kPBytes;                  // dQ staging: 4 boxes [64 q][32 fp32] (128B swizzle)
+constexpr int kDQBytes = BQ * D * 4;
+constexpr int kStats = kDQ + kDQBytes;                  // [STAGES][2][BQ] fp32 (LSE, D)
 constexpr int kBar = kStats + STAGES * 2 * BQ * 4;
 // bars: kv, q_full[ST], q_empty[ST], s_full, ds_ready, dq_full[2], dq_empty[2], acc_full
 constexpr int kNumBars = 1 + 2 * STAGES + 1 + 1 + 2 + 2 + 1;
@@ -63,14 +67,13 @@ struct Args {
   float dv_scale;     // s
   const float* lse;   // [hq][c]
   const float* Dv;    // [hq][c]
-  float* dqacc;       // [hq][c][D]
-  float* dkv;         // [2][hkv][S][D]
 };
 }  // namespace bwd
 
 __global__ void __launch_bounds__(bwd::kThreads, 1)
     seco_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                          const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv,
                           const bwd::Args a) {
   using namespace bwd;
   constexpr int BOX_KV = 128 * 128;  // [128 rows][128 B]
@@ -79,6 +82,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
   const uint32_t sK = sb + kK, sV = sb + kV, sQ = sb + kQ, sDO = sb + kDO, sP = sb + kP, sDS = sb + kDS;
+  const uint32_t sDQ = sb + kDQ;
   const float* stats = reinterpret_cast<const float*>(smem + kStats);
   const uint32_t sStats = sb + kStats;
   const uint32_t b0 = sb + kBar;
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   const int k0 = u * BKV;                                  // first key (absolute position)
   const int nqt = a.c / BQ;
   const int rel = k0 - a.j * a.c;                          // key offset relative to chunk j's first row
-  const int qt_min = rel > 0 ? (rel - (BQ - 1) + BQ - 1) / BQ : 0;
+  const int qt_min = rel > 0 ? rel / BQ : 0;              // first query tile that sees key k0
   const int n_all = a.G * (nqt - qt_min);
   const int it0 = (int)((int64_t)split * n_all / a.nsplit);
   const int it1 = (int)((int64_t)(split + 1) * n_all / a.nsplit);
@@ -121,6 +125,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_q); tma_prefetch(&tm_do); tma_prefetch(&tm_k); tma_prefetch(&tm_v);
+    tma_prefetch(&tm_dq); tma_prefetch(&tm_dkv);
   }
   if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
   tc_fence_before();
@@ -222,6 +227,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
       const int key_pos = k0 + kr;
       const float sl2 = a.scale_log2;
+      const f2_t sl2x2 = f2(sl2, sl2);
+      const f2_t nlog2e = f2(-1.4426950408889634f, -1.4426950408889634f);
       for (int i = 0; i < n; ++i) {
         const int st = i % STAGES, pb = i % 2;
         const int qt = iter_qt(i);
@@ -231,21 +238,32 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         uint32_t sv[32], dpv[32];
         tmem_ld32(tmem + lane_addr + TM_S + wg * 32, sv);
         tmem_ld32(tmem + lane_addr + TM_DP + wg * 32, dpv);
-        tmem_wait_ld();
-        const float* lse_s = stats + st * 2 * BQ + wg * 32;
-        const float* d_s = lse_s + BQ;
+        const float4* lse4 = reinterpret_cast<const float4*>(stats + st * 2 * BQ + wg * 32);
+        const float4* d4 = reinterpret_cast<const float4*>(stats + st * 2 * BQ + BQ + wg * 32);
         const int qpos0 = a.j * a.c + qt * BQ + wg * 32;  // absolute position of column 0
+        // causal mask only where this warp's keys can exceed this warpgroup's query positions
+        const bool masked = (k0 + wq * 32 + 31) > qpos0;
+        tmem_wait_ld();
         uint32_t pp[16], dd[16];
 #pragma unroll
-        for (int c2 = 0; c2 < 32; c2 += 2) {
-          float p0 = ex2(__uint_as_float(sv[c2]) * sl2 - lse_s[c2] * 1.4426950408889634f);
-          float p1 = ex2(__uint_as_float(sv[c2 + 1]) * sl2 - lse_s[c2 + 1] * 1.4426950408889634f);
-          if (key_pos > qpos0 + c2) p0 = 0.f;
-          if (key_pos > qpos0 + c2 + 1) p1 = 0.f;
-          const float ds0 = p0 * (__uint_as_float(dpv[c2]) - d_s[c2]);
-          const float ds1 = p1 * (__uint_as_float(dpv[c2 + 1]) - d_s[c2 + 1]);
-          pp[c2 / 2] = pack_bf16(p0, p1);
-          dd[c2 / 2] = pack_bf16(ds0, ds1);
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 L = lse4[c4], Dv = d4[c4];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const int c2 = c4 * 4 + hf * 2;
+            const f2_t lse2 = hf ? f2(L.z, L.w) : f2(L.x, L.y);
+            const f2_t dd2 = hf ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y);
+            const f2_t x = ffma2(f2u(sv[c2], sv[c2 + 1]), sl2x2, fmul2(lse2, nlog2e));
+            float p0 = ex2(f2lo(x)), p1 = ex2(f2hi(x));
+            if (masked) {
+              if (key_pos > qpos0 + c2) p0 = 0.f;
+              if (key_pos > qpos0 + c2 + 1) p1 = 0.f;
+            }
+            const f2_t p2 = f2(p0, p1);
+            const f2_t ds2 = fmul2(p2, fsub2(f2u(dpv[c2], dpv[c2 + 1]), dd2));
+            pp[c2 / 2] = pack_bf16(p0, p1);
+            dd[c2 / 2] = pack_bf16_f2(ds2);
+          }
         }
         const uint32_t prow = sP + pb * kPBytes, drow = sDS + pb * kPBytes;
 #pragma unroll
@@ -257,26 +275,42 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         tc_fence_before();
         mbar_arrive(bar_ds_ready);
       }
-      // final: dK (warpgroup 0) / dV (warpgroup 1) -> red.add into dkv
+      // final: dK (warpgroup 0) / dV (warpgroup 1): TMEM -> scaled fp32 in smem (128B-swizzled
+      // boxes [128 keys][32 fp32]) -> TMA reduce-add into dkv.  The Q/dO ring (dK) and the
+      // P/dS buffers (dV) are free once every MMA has completed (bar_acc).
       mbar_wait(bar_acc, 0);
       tc_fence_after();
       const float sc = wg == 0 ? a.dk_scale : a.dv_scale;
-      float* dst = a.dkv + ((int64_t)(wg * a.hkv + g) * a.S + key_pos) * D;
+      const uint32_t stg = wg == 0 ? sQ : sP;   // 64 KiB each, 1024-B aligned
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t v[32];
         tmem_ld32(tmem + lane_addr + (wg == 0 ? TM_DK : TM_DV) + cc * 32, v);
         tmem_wait_ld();
+        const uint32_t box = stg + cc * (BKV * 128);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          red_add_v4_f32(dst + cc * 32 + 4 * q, sc * __uint_as_float(v[4 * q]), sc * __uint_as_float(v[4 * q + 1]),
-                         sc * __uint_as_float(v[4 * q + 2]), sc * __uint_as_float(v[4 * q + 3]));
+          st_shared_v4(box + sw128_off(kr, q), __float_as_uint(sc * __uint_as_float(v[4 * q])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 1])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 2])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 3])));
+      }
+      fence_async_smem();
+      named_bar_sync(2 + wg, 128);
+      if (wq == 0 && lane == 0) {
+        const int row0 = (wg * a.hkv + g) * a.S + k0;
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg + cc * (BKV * 128), cc * 32, row0);
+        bulk_commit();
+        bulk_wait0();
       }
     } else if (warp >= 12) {
       // -------------------------------------------------------------- dQ drain
       const int wq = warp % 4;
-      const int dl = wq * 32 + lane;   // head-dim index (TMEM lane of dQ^T)
       const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+      const bool leader = (warp == 12 && lane == 0);
+      const uint32_t box = sDQ + wq * (BQ * 128);       // this warp's 32 head-dims
+      const uint32_t colb = (uint32_t)(lane & 3) * 4;
       for (int i = 0; i < n; ++i) {
         const int qb = i % 2;
         const int h = iter_h(i), qt = iter_qt(i);
@@ -288,12 +322,26 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(bar_dq_empty(qb));
-        float* base = a.dqacc + ((int64_t)h * a.c + qt * BQ) * D + dl;
+        if (leader) bulk_wait_read0();        // previous reduce has finished reading the staging tile
+        named_bar_sync(1, 128);
+        // element (q row, head-dim dl) -> box wq, row q, 16-B chunk (lane/4) ^ (q%8), word lane%4
 #pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2) red_add_f32(base + (int64_t)c2 * D, __uint_as_float(v0[c2]));
+        for (int q = 0; q < 32; ++q)
+          st_shared_f32(box + q * 128 + ((((uint32_t)lane >> 2) ^ (q & 7)) << 4) + colb, __uint_as_float(v0[q]));
 #pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2) red_add_f32(base + (int64_t)(32 + c2) * D, __uint_as_float(v1[c2]));
+        for (int q = 0; q < 32; ++q)
+          st_shared_f32(box + (32 + q) * 128 + ((((uint32_t)lane >> 2) ^ (q & 7)) << 4) + colb,
+                        __uint_as_float(v1[q]));
+        fence_async_smem();
+        named_bar_sync(1, 128);
+        if (leader) {
+          const int row0 = h * a.c + qt * BQ;
+#pragma unroll
+          for (int b = 0; b < D / 32; ++b) tma_reduce_add_2d(&tm_dq, sDQ + b * (BQ * 128), b * 32, row0);
+          bulk_commit();
+        }
       }
+      if (leader) bulk_wait0();
     }
   }
   __syncwarp();
@@ -304,7 +352,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
 }
 
 cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tdo,
-                             const CUtensorMap& tk, const CUtensorMap& tv, const void* o, const void* d_o,
+                             const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tdq,
+                             const CUtensorMap& tdkv, const void* o, const void* d_o,
                              const float* lse, float relay, float gscale, float* dkv, void* dq, void* dk_own,
                              void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st, int* launches) {
   static_assert(bwd::kAlloc <= 232448, "shared memory budget");
@@ -322,7 +371,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.dk_scale = gscale * g.scale;
   a.dv_scale = gscale;
-  a.lse = lse; a.Dv = ws_D; a.dqacc = ws_dqacc; a.dkv = dkv;
+  a.lse = lse; a.Dv = ws_D;
   const int ntiles = (g.j + 1) * g.c / bwd::BKV;
   // Q-split when the chunk offers fewer key tiles than ~2 waves of SMs; each split keeps
   // at least 2*G query tiles (the shortest diagonal tile has 2*G of them).
@@ -331,7 +380,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   if (nsplit < 1) nsplit = 1;
   a.nsplit = nsplit;
   dim3 grid(ntiles * nsplit * g.hkv);
-  seco_bwd_sm100_kernel<<<grid, bwd::kThreads, bwd::kAlloc, st>>>(tq, tdo, tk, tv, a);
+  seco_bwd_sm100_kernel<<<grid, bwd::kThreads, bwd::kAlloc, st>>>(tq, tdo, tk, tv, tdq, tdkv, a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   e = launch_final_bf16(g, ws_dqacc, dq, dkv, dk_own, dv_own, gscale * g.scale, st);
   *launches = 2 + 1;

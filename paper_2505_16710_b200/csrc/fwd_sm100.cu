@@ -181,21 +181,31 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     const uint32_t tO = tmem + lane_addr + NH * fwd::BN + b * D;
     const uint32_t pRow = sP + b * L::kPBytes;
     const float sl2 = a.scale_log2;
+    const f2_t sl2x2 = f2(sl2, sl2);
     float m = -INFINITY, l = 0.f;
     for (int t = 0; t < T; ++t) {
       mbar_wait(bar_s_full(b), t & 1);
       tc_fence_after();
-      const bool diag = (t == T - 1);
+      const bool diag = (t == T - 1);   // the only tile that needs the causal mask
+      // pass 1: row max of the raw logits
       float mx = -INFINITY;
+      if (!diag) {
 #pragma unroll
-      for (int cc = 0; cc < fwd::BN / 32; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tS + cc * 32, v);
-        tmem_wait_ld();
+        for (int cc = 0; cc < fwd::BN / 32; ++cc) {
+          uint32_t v[32];
+          tmem_ld32(tS + cc * 32, v);
+          tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float x = (diag && cc * 32 + i > r) ? -INFINITY : __uint_as_float(v[i]);
-          mx = fmaxf(mx, x);
+          for (int i = 0; i < 32; i += 2) mx = fmax3(mx, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        }
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < fwd::BN / 32; ++cc) {
+          uint32_t v[32];
+          tmem_ld32(tS + cc * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = (cc * 32 + i > r) ? mx : fmaxf(mx, __uint_as_float(v[i]));
         }
       }
       const float m_new = fmaxf(m, mx * sl2);
@@ -205,6 +215,9 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       l *= alpha;
       if (t > 0) mbar_wait(bar_o_full(b), (t - 1) & 1);  // PV_b(t-1) done: P_b smem and O_b free
       tc_fence_after();
+      // pass 2: P = exp2(S sigma log2e - m) -> bf16 -> smem (128B swizzle), row sum in fp32 pairs
+      const f2_t negm = f2(-m_use, -m_use);
+      f2_t lsum = f2(0.f, 0.f);
 #pragma unroll
       for (int cc = 0; cc < fwd::BN / 32; ++cc) {
         uint32_t v[32];
@@ -213,11 +226,14 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float p0 = ex2(__uint_as_float(v[i]) * sl2 - m_use);
-          float p1 = ex2(__uint_as_float(v[i + 1]) * sl2 - m_use);
-          if (diag && cc * 32 + i > r) p0 = 0.f;
-          if (diag && cc * 32 + i + 1 > r) p1 = 0.f;
-          l += p0 + p1;
+          const f2_t x = ffma2(f2u(v[i], v[i + 1]), sl2x2, negm);
+          float p0 = ex2(f2lo(x)), p1 = ex2(f2hi(x));
+          if (diag) {
+            if (cc * 32 + i > r) p0 = 0.f;
+            if (cc * 32 + i + 1 > r) p1 = 0.f;
+          }
+          const f2_t p2 = f2(p0, p1);
+          lsum = fadd2(lsum, p2);
           pk[i / 2] = pack_bf16(p0, p1);
         }
         // keys cc*32 .. cc*32+31 -> box (cc/2), 16-byte chunks (cc%2)*4 .. +3 of row r
@@ -227,6 +243,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           st_shared_v4(box + sw128_off(r, (cc % 2) * 4 + q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
                        pk[4 * q + 3]);
       }
+      l += f2lo(lsum) + f2hi(lsum);
       if (t > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {

@@ -26,7 +26,8 @@ cudaError_t launch_bwd_fp32(const ChunkGeom& g, const float* q, const float* k, 
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, void* o, float* lse, cudaStream_t st);
 cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tdo,
-                             const CUtensorMap& tk, const CUtensorMap& tv, const void* o, const void* d_o,
+                             const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tdq,
+                             const CUtensorMap& tdkv, const void* o, const void* d_o,
                              const float* lse, float relay, float gscale, float* dkv, void* dq,
                              void* dk_own, void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st,
                              int* launches);

@@ -64,6 +64,20 @@ bool encode_3d(CUtensorMap* m, const void* ptr, int d, int rows, int heads, int6
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D fp32 tensor map over a dense [rows][128] matrix, box {32, box_rows}, 128-B swizzle
+// (the TMA reduce-add targets: dQ accumulator and dKV)
+bool encode_f32_rows(CUtensorMap* m, const void* ptr, int64_t rows, int box_rows) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {128 * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 seco_status check_shape(const seco_shape* s, int32_t j) {
@@ -195,13 +209,16 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(d_o) || !aligned16(dq))
     return fail(SECO_ERR_ARG, "bf16 tensors must be 16-byte aligned");
   const int S_used = (j + 1) * s->chunk;
-  CUtensorMap tq, tdo, tk, tv;
+  CUtensorMap tq, tdo, tk, tv, tdq, tdkv;
+  const int64_t S = (int64_t)s->chunk * s->num_chunks;
   if (!encode_3d(&tq, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64) ||
       !encode_3d(&tdo, d_o, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64) ||
       !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
-      !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128))
+      !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
+      !encode_f32_rows(&tdq, ws_dqacc, (int64_t)s->hq * s->chunk, 64) ||
+      !encode_f32_rows(&tdkv, dkv, 2 * (int64_t)s->hkv * S, 128))
     return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  e = seco::launch_bwd_sm100(g, tq, tdo, tk, tv, o, d_o, lse, relay_scale, grad_scale, dkv, dq, dk_own, dv_own,
+  e = seco::launch_bwd_sm100(g, tq, tdo, tk, tv, tdq, tdkv, o, d_o, lse, relay_scale, grad_scale, dkv, dq, dk_own, dv_own,
                              ws_dqacc, ws_D, cs, &launches);
   if (e != cudaSuccess) return cuda_fail(e, "bwd_sm100");
   g_launches = launches;
