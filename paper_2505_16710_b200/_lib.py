@@ -7,7 +7,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libseco.so")
+LIB_PATH = os.path.join(_PKG, os.environ.get("SECO_LIB_VARIANT", "libseco.so"))
 
 SECO_OK, SECO_ERR_ARG, SECO_ERR_UNSUPPORTED, SECO_ERR_CUDA = 0, 1, 2, 3
 SECO_BF16, SECO_FP32_DEBUG = 0, 1

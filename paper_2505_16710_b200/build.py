@@ -43,7 +43,12 @@ def _run(cmd, verbose):
         print(r.stdout + r.stderr)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, trace: bool = False) -> str:
+    """Build libseco.so (or, with trace=True, the instrumented libseco_trace.so used by
+    tools/trace_bwd.py; never loaded by the product path)."""
+    global BUILD, LIB
+    if trace:
+        BUILD, LIB = BUILD + "_trace", LIB.replace("libseco.so", "libseco_trace.so")
     os.makedirs(BUILD, exist_ok=True)
     hdr_t = max(_mtime(h) for h in HEADERS)
     objs = []
@@ -52,7 +57,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
         op = os.path.join(BUILD, src + ".o")
         objs.append(op)
         if force or _mtime(op) < max(_mtime(sp), hdr_t):
-            flags = CU_FLAGS + (["-Xptxas", "-v"] if ptxas_info else [])
+            flags = CU_FLAGS + (["-Xptxas", "-v"] if ptxas_info else []) + (["-DSECO_TRACE"] if trace else [])
             if src.endswith(".cpp"):
                 cmd = [NVCC, "-x", "cu"] + flags + ["-c", sp, "-o", op]
             else:
@@ -68,5 +73,6 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas-info", action="store_true")
+    ap.add_argument("--trace", action="store_true")
     a = ap.parse_args()
-    print(build(a.force, a.verbose, a.ptxas_info))
+    print(build(a.force, a.verbose, a.ptxas_info, a.trace))

@@ -28,6 +28,11 @@
 
 namespace seco {
 
+#ifdef SECO_TRACE
+unsigned long long* seco_trace_buffer = nullptr;
+extern "C" void* seco_debug_trace_ptr() { return seco_trace_buffer; }
+#endif
+
 cudaError_t launch_prep_bf16(const ChunkGeom& g, const void* o, const void* d_o, float* D, float* dkv,
                              float* dqacc, float relay, cudaStream_t st);
 cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, const float* dkv, void* dk_own,
@@ -67,7 +72,9 @@ struct Args {
   float dv_scale;     // s
   const float* lse;   // [hq][c]
   const float* Dv;    // [hq][c]
+  unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters] clock64 stamps
 };
+constexpr int kTraceCtas = 4, kTraceSlots = 10, kTraceIters = 128;
 }  // namespace bwd
 
 __global__ void __launch_bounds__(bwd::kThreads, 1)
@@ -97,6 +104,15 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTmemSlot);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#ifdef SECO_TRACE
+#define TRACE(slot, i)                                                                                      \
+  do {                                                                                                      \
+    if (a.trace && blockIdx.x < kTraceCtas && (i) < kTraceIters)                                            \
+      a.trace[((size_t)blockIdx.x * kTraceSlots + (slot)) * kTraceIters + (i)] = clock64();                \
+  } while (0)
+#else
+#define TRACE(slot, i) do { } while (0)
+#endif
   // block -> (key tile u, split s, kv head g); key tiles in ascending order = longest work first
   const int bid = blockIdx.x;
   const int g = bid % a.hkv;
@@ -147,6 +163,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           const uint32_t ph = (i / STAGES) & 1;
           const int h = iter_h(i), qt = iter_qt(i);
           mbar_wait(bar_q_empty(st), ph ^ 1);
+          TRACE(0, i);
           mbar_expect_tx(bar_q_full(st), 2 * kQBytes + 2 * BQ * 4);
           for (int x = 0; x < D / 64; ++x) {
             tma_load_3d(sQ + st * kQBytes + x * BOX_Q, &tm_q, bar_q_full(st), x * 64, qt * BQ, h);
@@ -187,10 +204,12 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         for (int i = 0; i < n; ++i) {
           const int st = i % STAGES, pb = i % 2, qb = i % 2;
           mbar_wait(bar_ds_ready, i & 1);
+          TRACE(1, i);
           tc_fence_after();
           if (i + 1 < n) {
             const int st1 = (i + 1) % STAGES;
             mbar_wait(bar_q_full(st1), ((i + 1) / STAGES) & 1);
+            TRACE(2, i);
             tc_fence_after();
             issue_s_dp(st1);
             mma_commit(bar_s_full);
@@ -209,6 +228,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           mma_commit(bar_q_empty(st));
           // dQ^T = K^T dS^T
           mbar_wait(bar_dq_empty(qb), ((i / 2) & 1) ^ 1);
+          TRACE(3, i);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk) {
@@ -216,6 +236,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
                    make_desc_sw128(sDS + pb * kPBytes + kk * 2048, BOX_KV, 1024), idesc_q, kk > 0);
           }
           mma_commit(bar_dq_full(qb));
+          TRACE(4, i);
         }
         mma_commit(bar_acc);
       }
@@ -234,6 +255,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         const int qt = iter_qt(i);
         mbar_wait(bar_q_full(st), (i / STAGES) & 1);   // LSE / D of this tile are in smem
         mbar_wait(bar_s_full, i & 1);
+        if (lane == 0 && wq == 0 && wg == 0) TRACE(5, i);
         tc_fence_after();
         uint32_t sv[32], dpv[32];
         tmem_ld32(tmem + lane_addr + TM_S + wg * 32, sv);
@@ -273,6 +295,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         }
         fence_async_smem();
         tc_fence_before();
+        if (lane == 0 && wq == 0) TRACE(6 + 3 * wg, i);
         mbar_arrive(bar_ds_ready);
       }
       // final: dK (warpgroup 0) / dV (warpgroup 1): TMEM -> scaled fp32 in smem (128B-swizzled
@@ -315,6 +338,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         const int qb = i % 2;
         const int h = iter_h(i), qt = iter_qt(i);
         mbar_wait(bar_dq_full(qb), (i / 2) & 1);
+        if (leader) TRACE(7, i);
         tc_fence_after();
         uint32_t v0[32], v1[32];
         tmem_ld32(tmem + lane_addr + TM_DQ + qb * BQ, v0);
@@ -339,6 +363,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
 #pragma unroll
           for (int b = 0; b < D / 32; ++b) tma_reduce_add_2d(&tm_dq, sDQ + b * (BQ * 128), b * 32, row0);
           bulk_commit();
+          TRACE(8, i);
         }
       }
       if (leader) bulk_wait0();
@@ -372,6 +397,16 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   a.dk_scale = gscale * g.scale;
   a.dv_scale = gscale;
   a.lse = lse; a.Dv = ws_D;
+  a.trace = nullptr;
+#ifdef SECO_TRACE
+  {
+    static unsigned long long* tbuf = nullptr;
+    if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * bwd::kTraceCtas * bwd::kTraceSlots * bwd::kTraceIters);
+    cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * bwd::kTraceCtas * bwd::kTraceSlots * bwd::kTraceIters, st);
+    a.trace = tbuf;
+    seco_trace_buffer = tbuf;
+  }
+#endif
   const int ntiles = (g.j + 1) * g.c / bwd::BKV;
   // Q-split when the chunk offers fewer key tiles than ~2 waves of SMs; each split keeps
   // at least 2*G query tiles (the shortest diagonal tile has 2*G of them).

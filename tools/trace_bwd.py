@@ -1,0 +1,60 @@
+"""Per-role clock64 timeline of seco_bwd_sm100_kernel (needs libseco_trace.so, built with
+`python -m paper_2505_16710_b200.build --trace`).  Runs one chunk backward at the bench
+shape and prints, for the first traced CTAs, per-iteration intervals in SM cycles:
+  period   MMA: ds_ready(i) -> ds_ready(i+1)
+  s_lat    MMA got ds_ready(i-1) (issues S/dP(i)) -> compute sees s_full(i)
+  comp     compute: s_full(i) -> arrive ds_ready(i)   (WG0; WG1 in brackets)
+  dqwait   MMA: q_full(i+1) ok -> dq_empty(i) ok      (includes dV/dK issue)
+  drain    drain: dq_full(i) -> bulk reduce issued
+usage: SECO_LIB_VARIANT=libseco_trace.so python tools/trace_bwd.py [j] [cfg]"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("SECO_LIB_VARIANT", "libseco_trace.so")
+import numpy as np
+import torch
+
+from paper_2505_16710_b200 import _lib
+from paper_2505_16710_b200.step import ChunkedAttention
+
+j = int(sys.argv[1]) if len(sys.argv) > 1 else 15
+hq, hkv, d, S, c = 32, 8, 128, 32768, 2048
+torch.manual_seed(0)
+q = torch.randn(hq, S, d, device="cuda").bfloat16()
+k = torch.randn(hkv, S, d, device="cuda").bfloat16()
+v = torch.randn(hkv, S, d, device="cuda").bfloat16()
+do = torch.randn(hq, S, d, device="cuda").bfloat16()
+L = ChunkedAttention(hq, hkv, d, S, c)
+L.dkv.zero_()
+for rep in range(3):
+    L.forward_chunk(q, k, v, j)
+    L.backward_chunk(q, k, v, do, j)
+torch.cuda.synchronize()
+lib = _lib.load()
+lib.seco_debug_trace_ptr.restype = ctypes.c_void_p
+ptr = lib.seco_debug_trace_ptr()
+CT, SL, IT = 4, 10, 128
+host = np.zeros((CT, SL, IT), dtype=np.uint64)
+cudart = ctypes.CDLL("libcudart.so.12")
+cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+assert cudart.cudaMemcpy(host.ctypes.data, ptr, host.nbytes, 2) == 0
+t = host.astype(np.int64)
+for cta in range(2):
+    n = int((t[cta, 1] > 0).sum())
+    print(f"CTA {cta}: {n} iterations")
+    base = t[cta, 1, 0]
+    rows = []
+    for i in range(1, min(n, 40)):
+        period = t[cta, 1, i] - t[cta, 1, i - 1] if i < n else 0
+        s_lat = t[cta, 5, i] - t[cta, 1, i - 1]
+        comp = t[cta, 6, i] - t[cta, 5, i]
+        comp1 = t[cta, 9, i] - t[cta, 5, i]
+        dqw = t[cta, 3, i] - t[cta, 2, i] if t[cta, 2, i] else 0
+        drain = t[cta, 8, i] - t[cta, 7, i]
+        prod = t[cta, 0, i] - base if t[cta, 0, i] else 0
+        print(f"  i={i:3d} period={period:6d} s_lat={s_lat:6d} comp={comp:6d} [{comp1:6d}] dqwait={dqw:6d} "
+              f"drain={drain:6d} prod_t={prod:8d}")
+    per = np.diff(t[cta, 1, :n])
+    print(f"  mean period {per.mean():.0f} cycles over {n} iterations; MMA ideal 1280")
