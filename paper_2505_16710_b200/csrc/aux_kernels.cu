@@ -34,13 +34,15 @@ struct PrepArgs {
   int nD, nR, nZ;  // block counts of the three tasks
 };
 
-// Task A (blocks [0,nD)): one warp per (h, row): D = sum_x dO*O.
+// Task A (blocks [0,nD)): one warp per (h, row): D = sum_x dO*O (and -LSE log2 e for the
+// tensor-core kernel, which evaluates P = exp2(S sigma log2 e - LSE log2 e) with one FFMA).
 // Task B (blocks [nD,nD+nR)): scale slot j of dkv (both dK and dV) by relay.
 // Task C (rest): zero dQacc [hq][c][d].
 template <typename T>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, const T* __restrict__ d_o,
                                                        float* __restrict__ D, float* __restrict__ dkv,
-                                                       float* __restrict__ dqacc, PrepArgs a) {
+                                                       float* __restrict__ dqacc, const float* __restrict__ lse,
+                                                       float* __restrict__ nlse, PrepArgs a) {
   const int bid = blockIdx.x;
   if (bid < a.nD) {
     const int w = bid * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -51,7 +53,10 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
     float acc = 0.f;
     for (int x = lane; x < a.d; x += 32) acc += ldf(orow + x) * ldf(drow + x);
     acc = warp_sum(acc);
-    if (lane == 0) D[(int64_t)h * a.c + r] = acc;
+    if (lane == 0) {
+      D[(int64_t)h * a.c + r] = acc;
+      if (nlse) nlse[(int64_t)h * a.c + r] = -1.4426950408889634f * lse[(int64_t)h * a.c + r];
+    }
   } else if (bid < a.nD + a.nR) {
     if (a.relay == 1.f) return;
     const int64_t per = (int64_t)a.c * a.d;                 // one slot of one head
@@ -83,45 +88,63 @@ struct FinalArgs {
 };
 
 // Task A (blocks [0,nQ)): dq = T(dq_scale * dqacc) (skipped when dqacc == null).
-// Task B: dk_own / dv_own = T(dkv slot j).
+// Task B: dk_own / dv_own = T(dkv slot j).  Both move 4 consecutive elements per thread
+// step (d % 4 == 0 is required by the ABI), so index arithmetic is paid once per 4.
+template <typename T> struct Vec4;
+template <> struct Vec4<float> {
+  static SECO_DEV void store(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+};
+template <> struct Vec4<__nv_bfloat16> {
+  static SECO_DEV void store(__nv_bfloat16* p, float4 v) {
+    uint2 w;
+    w.x = pack_bf16(v.x, v.y);
+    w.y = pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(p) = w;
+  }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict__ dqacc, T* __restrict__ dq,
                                                         const float* __restrict__ dkv, T* __restrict__ dk_own,
                                                         T* __restrict__ dv_own, FinalArgs a) {
   const int bid = blockIdx.x;
+  const int dv4 = a.d / 4;
   if (bid < a.nQ) {
     if (dqacc == nullptr) return;
-    const int64_t total = (int64_t)a.hq * a.c * a.d;
-    for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < total; i += (int64_t)a.nQ * blockDim.x) {
-      const int64_t h = i / ((int64_t)a.c * a.d), rem = i % ((int64_t)a.c * a.d);
-      const int64_t r = rem / a.d, x = rem % a.d;
-      stf(dq + h * a.qh + r * a.qr + x, a.dq_scale * dqacc[i]);
+    const int64_t rows = (int64_t)a.hq * a.c;
+    for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < rows * dv4; i += (int64_t)a.nQ * blockDim.x) {
+      const int64_t row = i / dv4;
+      const int x = (int)(i - row * dv4) * 4;
+      const int64_t h = row / a.c, r = row - h * a.c;
+      float4 v = reinterpret_cast<const float4*>(dqacc)[i];
+      v.x *= a.dq_scale; v.y *= a.dq_scale; v.z *= a.dq_scale; v.w *= a.dq_scale;
+      Vec4<T>::store(dq + h * a.qh + r * a.qr + x, v);
     }
   } else {
     if (dk_own == nullptr && dv_own == nullptr) return;
-    const int64_t per = (int64_t)a.c * a.d;
-    const int64_t total = 2 * (int64_t)a.hkv * per;
+    const int64_t per4 = (int64_t)a.c * dv4;          // one slot of one head, in float4 units
+    const int64_t total = 2 * (int64_t)a.hkv * per4;
     for (int64_t i = (int64_t)(bid - a.nQ) * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)a.nO * blockDim.x) {
-      const int64_t th = i / per, off = i % per;
+      const int64_t th = i / per4, off4 = i - th * per4;
       const int t = (int)(th / a.hkv), g = (int)(th % a.hkv);
-      const float v = dkv[th * (int64_t)a.S * a.d + (int64_t)a.j * per + off];
+      const float4 v = reinterpret_cast<const float4*>(dkv + th * (int64_t)a.S * a.d + (int64_t)a.j * a.c * a.d)[off4];
       T* dst = t == 0 ? dk_own : dv_own;
-      if (dst) stf(dst + (int64_t)g * per + off, v);
+      if (dst) Vec4<T>::store(dst + (int64_t)g * a.c * a.d + off4 * 4, v);
     }
   }
 }
 
 template <typename T>
 static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, float* D, float* dkv, float* dqacc,
-                               float relay, cudaStream_t st) {
+                               const float* lse, float* nlse, float relay, cudaStream_t st) {
   PrepArgs a;
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
   a.qh = g.qh; a.qr = g.qr; a.relay = relay;
   a.nD = (g.hq * g.c + 7) / 8;
   a.nR = relay == 1.f ? 0 : 296;
   a.nZ = dqacc ? 296 : 0;
-  bwd_prep_kernel<T><<<a.nD + a.nR + a.nZ, 256, 0, st>>>(o, d_o, D, dkv, dqacc, a);
+  bwd_prep_kernel<T><<<a.nD + a.nR + a.nZ, 256, 0, st>>>(o, d_o, D, dkv, dqacc, lse, nlse, a);
   return cudaGetLastError();
 }
 
@@ -140,9 +163,10 @@ static cudaError_t launch_final(const ChunkGeom& g, const float* dqacc, T* dq, c
 
 // bf16 path helpers, used by launch_bwd_sm100
 cudaError_t launch_prep_bf16(const ChunkGeom& g, const void* o, const void* d_o, float* D, float* dkv,
-                             float* dqacc, float relay, cudaStream_t st) {
+                             float* dqacc, const float* lse, float* nlse, float relay, cudaStream_t st) {
   return launch_prep<__nv_bfloat16>(g, reinterpret_cast<const __nv_bfloat16*>(o),
-                                    reinterpret_cast<const __nv_bfloat16*>(d_o), D, dkv, dqacc, relay, st);
+                                    reinterpret_cast<const __nv_bfloat16*>(d_o), D, dkv, dqacc, lse, nlse, relay,
+                                    st);
 }
 cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, const float* dkv, void* dk_own,
                               void* dv_own, float dq_scale, cudaStream_t st) {
@@ -329,7 +353,7 @@ cudaError_t launch_fwd_fp32(const ChunkGeom& g, const float* q, const float* k, 
 cudaError_t launch_bwd_fp32(const ChunkGeom& g, const float* q, const float* k, const float* v, const float* o,
                             const float* d_o, const float* lse, float relay, float gscale, float* dkv, float* dq,
                             float* dk_own, float* dv_own, float* ws_D, cudaStream_t st, int* launches) {
-  cudaError_t e = launch_prep<float>(g, o, d_o, ws_D, dkv, nullptr, relay, st);
+  cudaError_t e = launch_prep<float>(g, o, d_o, ws_D, dkv, nullptr, lse, nullptr, relay, st);
   if (e != cudaSuccess) return e;
   DbgArgs a = dbg_args(g);
   dim3 gq((g.c + 7) / 8, g.hq);

@@ -34,7 +34,7 @@ extern "C" void* seco_debug_trace_ptr() { return seco_trace_buffer; }
 #endif
 
 cudaError_t launch_prep_bf16(const ChunkGeom& g, const void* o, const void* d_o, float* D, float* dkv,
-                             float* dqacc, float relay, cudaStream_t st);
+                             float* dqacc, const float* lse, float* nlse, float relay, cudaStream_t st);
 cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, const float* dkv, void* dk_own,
                               void* dv_own, float dq_scale, cudaStream_t st);
 
@@ -70,8 +70,8 @@ struct Args {
   float scale_log2;   // sigma * log2 e
   float dk_scale;     // s * sigma
   float dv_scale;     // s
-  const float* lse;   // [hq][c]
-  const float* Dv;    // [hq][c]
+  const float* nlse;  // [hq][c]  -LSE * log2(e)   (from bwd_prep)
+  const float* Dv;    // [hq][c]  rowsum(dO o O)  (from bwd_prep)
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters] clock64 stamps
 };
 constexpr int kTraceCtas = 4, kTraceSlots = 10, kTraceIters = 128;
@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   const uint32_t sb = smem_u32(smem);
   const uint32_t sK = sb + kK, sV = sb + kV, sQ = sb + kQ, sDO = sb + kDO, sP = sb + kP, sDS = sb + kDS;
   const uint32_t sDQ = sb + kDQ;
-  const float* stats = reinterpret_cast<const float*>(smem + kStats);
   const uint32_t sStats = sb + kStats;
   const uint32_t b0 = sb + kBar;
   const uint32_t bar_kv = b0;
@@ -126,9 +125,13 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   const int it0 = (int)((int64_t)split * n_all / a.nsplit);
   const int it1 = (int)((int64_t)(split + 1) * n_all / a.nsplit);
   const int n = it1 - it0;
-  // iteration i (0-based within this CTA) -> (q-head, query tile)
-  auto iter_h = [&](int i) { return g * a.G + (it0 + i) % a.G; };
-  auto iter_qt = [&](int i) { return qt_min + (it0 + i) / a.G; };
+  // iteration i (0-based within this CTA) -> (q-head, query tile): it = it0 + i,
+  // head = g*G + it % G, tile = qt_min + it / G; each role walks it incrementally
+  struct Walk {
+    int hh, qt, G;
+    __device__ void next() { if (++hh == G) { hh = 0; ++qt; } }
+  };
+  const Walk walk0{it0 % a.G, qt_min + it0 / a.G, a.G};
 
   if (threadIdx.x == 0) {
     mbar_init(bar_kv, 1);
@@ -158,10 +161,11 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           tma_load_3d(sK + x * BOX_KV, &tm_k, bar_kv, x * 64, k0, g);
           tma_load_3d(sV + x * BOX_KV, &tm_v, bar_kv, x * 64, k0, g);
         }
-        for (int i = 0; i < n; ++i) {
+        Walk w = walk0;
+        for (int i = 0; i < n; ++i, w.next()) {
           const int st = i % STAGES;
           const uint32_t ph = (i / STAGES) & 1;
-          const int h = iter_h(i), qt = iter_qt(i);
+          const int h = g * a.G + w.hh, qt = w.qt;
           mbar_wait(bar_q_empty(st), ph ^ 1);
           TRACE(0, i);
           mbar_expect_tx(bar_q_full(st), 2 * kQBytes + 2 * BQ * 4);
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
             tma_load_3d(sDO + st * kQBytes + x * BOX_Q, &tm_do, bar_q_full(st), x * 64, qt * BQ, h);
           }
           const int64_t ro = (int64_t)h * a.c + qt * BQ;
-          bulk_load(sStats + st * 2 * BQ * 4, a.lse + ro, BQ * 4, bar_q_full(st));
+          bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_q_full(st));
           bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_q_full(st));
         }
       }
@@ -249,42 +253,54 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       const int key_pos = k0 + kr;
       const float sl2 = a.scale_log2;
       const f2_t sl2x2 = f2(sl2, sl2);
-      const f2_t nlog2e = f2(-1.4426950408889634f, -1.4426950408889634f);
-      for (int i = 0; i < n; ++i) {
+      Walk w = walk0;
+      for (int i = 0; i < n; ++i, w.next()) {
         const int st = i % STAGES, pb = i % 2;
-        const int qt = iter_qt(i);
-        mbar_wait(bar_q_full(st), (i / STAGES) & 1);   // LSE / D of this tile are in smem
+        const int qt = w.qt;
+        mbar_wait(bar_q_full(st), (i / STAGES) & 1);   // -LSE log2e / D of this tile are in smem
         mbar_wait(bar_s_full, i & 1);
         if (lane == 0 && wq == 0 && wg == 0) TRACE(5, i);
         tc_fence_after();
         uint32_t sv[32], dpv[32];
         tmem_ld32(tmem + lane_addr + TM_S + wg * 32, sv);
         tmem_ld32(tmem + lane_addr + TM_DP + wg * 32, dpv);
-        const float4* lse4 = reinterpret_cast<const float4*>(stats + st * 2 * BQ + wg * 32);
-        const float4* d4 = reinterpret_cast<const float4*>(stats + st * 2 * BQ + BQ + wg * 32);
+        const uint32_t nl_s = sStats + (st * 2 * BQ + wg * 32) * 4;
+        const uint32_t d_s = nl_s + BQ * 4;
         const int qpos0 = a.j * a.c + qt * BQ + wg * 32;  // absolute position of column 0
         // causal mask only where this warp's keys can exceed this warpgroup's query positions
         const bool masked = (k0 + wq * 32 + 31) > qpos0;
         tmem_wait_ld();
         uint32_t pp[16], dd[16];
+        if (!masked) {
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 L = lse4[c4], Dv = d4[c4];
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 L = ld_shared_f4(nl_s + c4 * 16), Dv = ld_shared_f4(d_s + c4 * 16);
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            const int c2 = c4 * 4 + hf * 2;
-            const f2_t lse2 = hf ? f2(L.z, L.w) : f2(L.x, L.y);
-            const f2_t dd2 = hf ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y);
-            const f2_t x = ffma2(f2u(sv[c2], sv[c2 + 1]), sl2x2, fmul2(lse2, nlog2e));
-            float p0 = ex2(f2lo(x)), p1 = ex2(f2hi(x));
-            if (masked) {
+            for (int hf = 0; hf < 2; ++hf) {
+              const int c2 = c4 * 4 + hf * 2;
+              const f2_t x = ffma2(f2u(sv[c2], sv[c2 + 1]), sl2x2, hf ? f2(L.z, L.w) : f2(L.x, L.y));
+              const f2_t p2 = f2(ex2(f2lo(x)), ex2(f2hi(x)));
+              const f2_t ds2 = fmul2(p2, fsub2(f2u(dpv[c2], dpv[c2 + 1]), hf ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y)));
+              pp[c2 / 2] = pack_bf16_f2(p2);
+              dd[c2 / 2] = pack_bf16_f2(ds2);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 L = ld_shared_f4(nl_s + c4 * 16), Dv = ld_shared_f4(d_s + c4 * 16);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const int c2 = c4 * 4 + hf * 2;
+              const f2_t x = ffma2(f2u(sv[c2], sv[c2 + 1]), sl2x2, hf ? f2(L.z, L.w) : f2(L.x, L.y));
+              float p0 = ex2(f2lo(x)), p1 = ex2(f2hi(x));
               if (key_pos > qpos0 + c2) p0 = 0.f;
               if (key_pos > qpos0 + c2 + 1) p1 = 0.f;
+              const f2_t p2 = f2(p0, p1);
+              const f2_t ds2 = fmul2(p2, fsub2(f2u(dpv[c2], dpv[c2 + 1]), hf ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y)));
+              pp[c2 / 2] = pack_bf16_f2(p2);
+              dd[c2 / 2] = pack_bf16_f2(ds2);
             }
-            const f2_t p2 = f2(p0, p1);
-            const f2_t ds2 = fmul2(p2, fsub2(f2u(dpv[c2], dpv[c2 + 1]), dd2));
-            pp[c2 / 2] = pack_bf16(p0, p1);
-            dd[c2 / 2] = pack_bf16_f2(ds2);
           }
         }
         const uint32_t prow = sP + pb * kPBytes, drow = sDS + pb * kPBytes;
@@ -334,9 +350,10 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       const bool leader = (warp == 12 && lane == 0);
       const uint32_t box = sDQ + wq * (BQ * 128);       // this warp's 32 head-dims
       const uint32_t colb = (uint32_t)(lane & 3) * 4;
-      for (int i = 0; i < n; ++i) {
+      Walk w = walk0;
+      for (int i = 0; i < n; ++i, w.next()) {
         const int qb = i % 2;
-        const int h = iter_h(i), qt = iter_qt(i);
+        const int h = g * a.G + w.hh, qt = w.qt;
         mbar_wait(bar_dq_full(qb), (i / 2) & 1);
         if (leader) TRACE(7, i);
         tc_fence_after();
@@ -383,7 +400,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st, int* launches) {
   static_assert(bwd::kAlloc <= 232448, "shared memory budget");
   if (g.d != bwd::D) return cudaErrorInvalidValue;
-  cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, relay, st);
+  cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.c, relay, st);
   if (e != cudaSuccess) return e;
   static bool attr_set = false;
   if (!attr_set) {
@@ -396,7 +413,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.dk_scale = gscale * g.scale;
   a.dv_scale = gscale;
-  a.lse = lse; a.Dv = ws_D;
+  a.nlse = ws_D + (size_t)g.hq * g.c; a.Dv = ws_D;
   a.trace = nullptr;
 #ifdef SECO_TRACE
   {

@@ -92,6 +92,15 @@ SECO_DEV void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem desc]^T  (A in tensor memory: lane = row, 2 bf16 per column)
+SECO_DEV void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
 // arrive (once) on an mbarrier when all previously issued tcgen05.mma of this thread complete
 SECO_DEV void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -124,6 +133,14 @@ SECO_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
       "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, "
       "%32};" ::"r"(taddr),
       SECO_W32(r)
+      : "memory");
+}
+SECO_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
 SECO_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -220,6 +237,22 @@ SECO_DEV f2_t fmul2(f2_t a, f2_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// 2^x for a pair on the FMA pipe (offloads the MUFU unit): Cody-Waite split x = j + f,
+// j = rint(x) via the 1.5*2^23 shifter, f in [-0.5, 0.5], 2^f by a degree-3 polynomial at
+// Chebyshev nodes (max rel. error 1.0e-4, far below bf16's 3.9e-3), then j added to the
+// exponent field.  x is clamped to >= -127 (the result underflows to ~0 there).
+SECO_DEV f2_t ex2_emu2(f2_t x) {
+  const f2_t xc = f2(fmaxf(f2lo(x), -127.f), fmaxf(f2hi(x), -127.f));
+  const f2_t magic = f2(12582912.f, 12582912.f);
+  const f2_t y = fadd2(xc, magic);
+  const f2_t f = fsub2(xc, fsub2(y, magic));
+  f2_t p = ffma2(f2(0.05583828315138817f, 0.05583828315138817f), f, f2(0.2426394820213318f, 0.2426394820213318f));
+  p = ffma2(p, f, f2(0.6931367516517639f, 0.6931367516517639f));
+  p = ffma2(p, f, f2(0.9999245405197144f, 0.9999245405197144f));
+  const uint32_t r0 = (uint32_t)p + ((uint32_t)y << 23);
+  const uint32_t r1 = (uint32_t)(p >> 32) + ((uint32_t)(y >> 32) << 23);
+  return f2u(r0, r1);
+}
 // bf16x2 pack of a pair (lo in the low half)
 SECO_DEV uint32_t pack_bf16_f2(f2_t v) { return pack_bf16(f2lo(v), f2hi(v)); }
 
@@ -234,6 +267,11 @@ SECO_DEV void tma_reduce_add_2d(const CUtensorMap* m, uint32_t src, int c0, int 
 SECO_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 SECO_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 SECO_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+SECO_DEV float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
 SECO_DEV void st_shared_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }

@@ -6,14 +6,18 @@
 // group (GQA: the NH tiles share every K/V tile loaded into shared memory).
 // Warp roles (warp-uniform dispatch):
 //   warp 0        TMA producer: Q tiles once, then K_t, V_t through a STAGES-deep ring
-//   warp 1        MMA issuer (one thread): S_b = Q_b K_t^T and O_b += P_b V_t (tcgen05.mma)
+//   warp 1        MMA issuer (one thread): S_b = Q_b K_t^T (SS) and O_b += P_b V_t (TS: P_b
+//                 is read straight from tensor memory)
 //   warp 2        TMEM allocator
 //   warps 4..     one 128-thread softmax warpgroup per q-head tile b (thread = query row):
-//                 tcgen05.ld S_b, online softmax in the log2 domain, P_b -> smem (bf16,
-//                 128B swizzle), lazy O rescale in TMEM, epilogue O/l -> global, LSE.
+//                 tcgen05.ld S_b, online softmax in the log2 domain, P_b (bf16) written back
+//                 over S_b's first 64 TMEM columns with tcgen05.st, lazy O rescale in TMEM,
+//                 epilogue O/l -> global, LSE.  A fixed share of the exponentials runs as a
+//                 polynomial on the FMA pipe (ex2_emu2) to relieve the MUFU unit.
 // MMA issue order ping-pongs the NH tiles: PV_0(t), S_0(t+1), PV_1(t), S_1(t+1), ...
-// so softmax of one tile overlaps tensor-core work of the other.
-// TMEM: S_b at columns [128b, 128b+128), O_b at [128 NH + D b, ... + D).
+// so the softmax of one tile overlaps tensor-core work of the other.  S_b(t+1) may
+// overwrite P_b(t) because tcgen05.mma from one thread executes in issue order.
+// TMEM: S_b / P_b at columns [128b, 128b+128), O_b at [128 NH + D b, ... + D).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -23,15 +27,14 @@ namespace fwd {
 constexpr int BM = 128;  // query rows per tile (= UMMA M)
 constexpr int BN = 128;  // keys per K/V tile (= UMMA N of S, K of PV)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
+constexpr int kEmuPairs = 5;               // of every 16 column pairs, this many use ex2_emu2
 
 template <int NH, int D, int STAGES>
 struct Layout {
   static constexpr int kTileBytes = BM * D * 2;       // Q tile, K tile, V tile (bf16)
-  static constexpr int kPBytes = BM * BN * 2;         // P tile (bf16)
   static constexpr int kQ = 0;
   static constexpr int kKV = kQ + NH * kTileBytes;
-  static constexpr int kP = kKV + STAGES * kTileBytes;
-  static constexpr int kBar = kP + NH * kPBytes;
+  static constexpr int kBar = kKV + STAGES * kTileBytes;
   // barriers: q[NH], kv_full[STAGES], kv_empty[STAGES], s_full[NH], p_full[NH], o_full[NH]
   static constexpr int kNumBars = NH + 2 * STAGES + 3 * NH;
   static constexpr int kTmemSlot = kBar + 8 * kNumBars;
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sQ = sbase + L::kQ, sKV = sbase + L::kKV, sP = sbase + L::kP;
+  const uint32_t sQ = sbase + L::kQ, sKV = sbase + L::kKV;
   const uint32_t bar0 = sbase + L::kBar;
   auto bar_q = [&](int b) { return bar0 + 8u * b; };
   auto bar_kv_full = [&](int s) { return bar0 + 8u * (NH + s); };
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(fwd::BM, fwd::BN, 0, 0);  // Q K-major, K K-major
-      constexpr uint32_t idesc_pv = make_idesc_bf16(fwd::BM, D, 0, 1);       // P K-major, V MN-major
+      constexpr uint32_t idesc_pv = make_idesc_bf16(fwd::BM, D, 0, 1);       // P (TMEM) K-major, V MN-major
       auto issue_s = [&](int b, int slot) {
         const uint32_t qa = sQ + b * L::kTileBytes, ka = sKV + slot * L::kTileBytes;
 #pragma unroll
@@ -130,12 +133,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         }
       };
       auto issue_pv = [&](int b, int slot, bool acc) {
-        const uint32_t pa = sP + b * L::kPBytes, va = sKV + slot * L::kTileBytes;
+        const uint32_t va = sKV + slot * L::kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < fwd::BN / 16; ++kk) {
-          const uint64_t ad = make_desc_sw128(pa + (kk / 4) * BOX + (kk % 4) * 32, 16, 1024);
           const uint64_t bd = make_desc_sw128(va + kk * 2048, BOX, 1024);
-          mma_ss(tmem + NH * fwd::BN + b * D, ad, bd, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+          mma_ts(tmem + NH * fwd::BN + b * D, tmem + b * fwd::BN + kk * 8, bd, idesc_pv, (acc || kk > 0) ? 1u : 0u);
         }
       };
       for (int b = 0; b < NH; ++b) mbar_wait(bar_q(b), 0);
@@ -179,7 +181,6 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
     const uint32_t tS = tmem + lane_addr + b * fwd::BN;
     const uint32_t tO = tmem + lane_addr + NH * fwd::BN + b * D;
-    const uint32_t pRow = sP + b * L::kPBytes;
     const float sl2 = a.scale_log2;
     const f2_t sl2x2 = f2(sl2, sl2);
     float m = -INFINITY, l = 0.f;
@@ -213,9 +214,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       const float m_use = need ? m_new : m;
       const float alpha = need ? ex2(m - m_new) : 1.f;
       l *= alpha;
-      if (t > 0) mbar_wait(bar_o_full(b), (t - 1) & 1);  // PV_b(t-1) done: P_b smem and O_b free
-      tc_fence_after();
-      // pass 2: P = exp2(S sigma log2e - m) -> bf16 -> smem (128B swizzle), row sum in fp32 pairs
+      // pass 2: P = exp2(S sigma log2e - m) -> bf16 -> TMEM columns [16cc, 16cc+16) of S_b's
+      // block (chunk cc only overwrites S columns this thread has already read)
       const f2_t negm = f2(-m_use, -m_use);
       f2_t lsum = f2(0.f, 0.f);
 #pragma unroll
@@ -227,24 +227,27 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           const f2_t x = ffma2(f2u(v[i], v[i + 1]), sl2x2, negm);
-          float p0 = ex2(f2lo(x)), p1 = ex2(f2hi(x));
+          f2_t p2;
+          if ((i / 2) < fwd::kEmuPairs) {
+            p2 = ex2_emu2(x);
+          } else {
+            p2 = f2(ex2(f2lo(x)), ex2(f2hi(x)));
+          }
           if (diag) {
+            float p0 = f2lo(p2), p1 = f2hi(p2);
             if (cc * 32 + i > r) p0 = 0.f;
             if (cc * 32 + i + 1 > r) p1 = 0.f;
+            p2 = f2(p0, p1);
           }
-          const f2_t p2 = f2(p0, p1);
           lsum = fadd2(lsum, p2);
-          pk[i / 2] = pack_bf16(p0, p1);
+          pk[i / 2] = pack_bf16_f2(p2);
         }
-        // keys cc*32 .. cc*32+31 -> box (cc/2), 16-byte chunks (cc%2)*4 .. +3 of row r
-        const uint32_t box = pRow + (cc / 2) * BOX;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          st_shared_v4(box + sw128_off(r, (cc % 2) * 4 + q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
-                       pk[4 * q + 3]);
+        tmem_st16(tS + cc * 16, pk);
       }
       l += f2lo(lsum) + f2hi(lsum);
       if (t > 0 && __any_sync(0xffffffffu, need)) {
+        mbar_wait(bar_o_full(b), (t - 1) & 1);  // PV_b(t-1) complete: O_b stable
+        tc_fence_after();
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {
           uint32_t v[32];
@@ -254,10 +257,9 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
           tmem_st32(tO + cc * 32, v);
         }
-        tmem_wait_st();
       }
+      tmem_wait_st();
       m = m_use;
-      fence_async_smem();
       tc_fence_before();
       mbar_arrive(bar_p_full(b));
     }
@@ -318,12 +320,8 @@ cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              const CUtensorMap& tv, void* o, float* lse, cudaStream_t st) {
   const int G = g.hq / g.hkv;
   if (g.d == 128) {
-    if (G % 2 == 0) return launch_fwd_impl<2, 128, 3>(g, tq, tk, tv, o, lse, st);
-    return launch_fwd_impl<1, 128, 4>(g, tq, tk, tv, o, lse, st);
-  }
-  if (g.d == 64) {
-    if (G % 2 == 0) return launch_fwd_impl<2, 64, 4>(g, tq, tk, tv, o, lse, st);
-    return launch_fwd_impl<1, 64, 4>(g, tq, tk, tv, o, lse, st);
+    if (G % 2 == 0) return launch_fwd_impl<2, 128, 5>(g, tq, tk, tv, o, lse, st);
+    return launch_fwd_impl<1, 128, 6>(g, tq, tk, tv, o, lse, st);
   }
   return cudaErrorInvalidValue;
 }

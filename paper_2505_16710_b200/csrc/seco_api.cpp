@@ -113,7 +113,8 @@ seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
 }
 
 size_t ws_floats(const seco_shape* s) {
-  return (size_t)s->hq * s->chunk * s->d + (size_t)s->hq * s->chunk;
+  // dQ accumulator [hq][c][d] + D [hq][c] + (-LSE log2 e) [hq][c]
+  return (size_t)s->hq * s->chunk * s->d + 2 * (size_t)s->hq * s->chunk;
 }
 
 // ---- splitmix64 (Steele, Lea & Flood 2014), state = seed
