@@ -27,7 +27,7 @@ namespace fwd {
 constexpr int BM = 128;  // query rows per tile (= UMMA M)
 constexpr int BN = 128;  // keys per K/V tile (= UMMA N of S, K of PV)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
-constexpr int kEmuPairs = 5;               // of every 16 column pairs, this many use ex2_emu2
+constexpr int kEmuPairs = 3;               // of every 16 column pairs, this many use ex2_emu2
 
 template <int NH, int D, int STAGES>
 struct Layout {
@@ -188,62 +188,49 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       mbar_wait(bar_s_full(b), t & 1);
       tc_fence_after();
       const bool diag = (t == T - 1);   // the only tile that needs the causal mask
-      // pass 1: row max of the raw logits
-      float mx = -INFINITY;
-      if (!diag) {
+      // single pass: the whole 128-column row of S_b in registers (4 loads, one wait)
+      uint32_t v[fwd::BN];
 #pragma unroll
-        for (int cc = 0; cc < fwd::BN / 32; ++cc) {
-          uint32_t v[32];
-          tmem_ld32(tS + cc * 32, v);
-          tmem_wait_ld();
+      for (int cc = 0; cc < fwd::BN / 32; ++cc) tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cc * 32));
+      tmem_wait_ld();
+      if (diag) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) mx = fmax3(mx, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
-        }
-      } else {
-#pragma unroll
-        for (int cc = 0; cc < fwd::BN / 32; ++cc) {
-          uint32_t v[32];
-          tmem_ld32(tS + cc * 32, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mx = (cc * 32 + i > r) ? mx : fmaxf(mx, __uint_as_float(v[i]));
-        }
+        for (int i = 0; i < fwd::BN; ++i)
+          if (i > r) v[i] = __float_as_uint(-INFINITY);
       }
-      const float m_new = fmaxf(m, mx * sl2);
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < fwd::BN; i += 4) {
+        mx0 = fmax3(mx0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+      }
+      const float m_new = fmaxf(m, fmaxf(mx0, mx1) * sl2);
       const bool need = m_new > m + fwd::kRescaleThreshold;
       const float m_use = need ? m_new : m;
       const float alpha = need ? ex2(m - m_new) : 1.f;
       l *= alpha;
-      // pass 2: P = exp2(S sigma log2e - m) -> bf16 -> TMEM columns [16cc, 16cc+16) of S_b's
-      // block (chunk cc only overwrites S columns this thread has already read)
+      // P = exp2(S sigma log2e - m) -> bf16 -> TMEM columns [16cc, 16cc+16) of S_b's block
+      // (masked entries hold -inf and give exactly 0)
       const f2_t negm = f2(-m_use, -m_use);
-      f2_t lsum = f2(0.f, 0.f);
+      f2_t lsum0 = f2(0.f, 0.f), lsum1 = f2(0.f, 0.f);
 #pragma unroll
       for (int cc = 0; cc < fwd::BN / 32; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tS + cc * 32, v);
-        tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const f2_t x = ffma2(f2u(v[i], v[i + 1]), sl2x2, negm);
+          const f2_t x = ffma2(f2u(v[cc * 32 + i], v[cc * 32 + i + 1]), sl2x2, negm);
           f2_t p2;
-          if ((i / 2) < fwd::kEmuPairs) {
+          if ((i / 2) < fwd::kEmuPairs && !diag) {   // masked (-inf) entries take MUFU: exact 0
             p2 = ex2_emu2(x);
           } else {
             p2 = f2(ex2(f2lo(x)), ex2(f2hi(x)));
           }
-          if (diag) {
-            float p0 = f2lo(p2), p1 = f2hi(p2);
-            if (cc * 32 + i > r) p0 = 0.f;
-            if (cc * 32 + i + 1 > r) p1 = 0.f;
-            p2 = f2(p0, p1);
-          }
-          lsum = fadd2(lsum, p2);
+          if ((i / 2) & 1) lsum1 = fadd2(lsum1, p2); else lsum0 = fadd2(lsum0, p2);
           pk[i / 2] = pack_bf16_f2(p2);
         }
         tmem_st16(tS + cc * 16, pk);
       }
+      const f2_t lsum = fadd2(lsum0, lsum1);
       l += f2lo(lsum) + f2hi(lsum);
       if (t > 0 && __any_sync(0xffffffffu, need)) {
         mbar_wait(bar_o_full(b), (t - 1) & 1);  // PV_b(t-1) complete: O_b stable
