@@ -49,6 +49,11 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, 
     global BUILD, LIB
     if trace:
         BUILD, LIB = BUILD + "_trace", LIB.replace("libseco.so", "libseco_trace.so")
+    # experiment variants: SECO_VARIANT=<name> SECO_DEFINES="-DX=1 ..." -> libseco_<name>.so
+    variant = os.environ.get("SECO_VARIANT")
+    extra = os.environ.get("SECO_DEFINES", "").split()
+    if variant:
+        BUILD, LIB = BUILD + "_" + variant, LIB.replace("libseco.so", f"libseco_{variant}.so")
     os.makedirs(BUILD, exist_ok=True)
     hdr_t = max(_mtime(h) for h in HEADERS)
     objs = []
@@ -57,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, 
         op = os.path.join(BUILD, src + ".o")
         objs.append(op)
         if force or _mtime(op) < max(_mtime(sp), hdr_t):
-            flags = CU_FLAGS + (["-Xptxas", "-v"] if ptxas_info else []) + (["-DSECO_TRACE"] if trace else [])
+            flags = CU_FLAGS + (["-Xptxas", "-v"] if ptxas_info else []) + (["-DSECO_TRACE"] if trace else []) + extra
             if src.endswith(".cpp"):
                 cmd = [NVCC, "-x", "cu"] + flags + ["-c", sp, "-o", op]
             else:

@@ -18,16 +18,26 @@
 // so the softmax of one tile overlaps tensor-core work of the other.  S_b(t+1) may
 // overwrite P_b(t) because tcgen05.mma from one thread executes in issue order.
 // TMEM: S_b / P_b at columns [128b, 128b+128), O_b at [128 NH + D b, ... + D).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace seco {
 
+#ifdef SECO_TRACE
+unsigned long long* seco_fwd_trace_buffer = nullptr;
+extern "C" void* seco_debug_fwd_trace_ptr() { return seco_fwd_trace_buffer; }
+#endif
+
 namespace fwd {
 constexpr int BM = 128;  // query rows per tile (= UMMA M)
 constexpr int BN = 128;  // keys per K/V tile (= UMMA N of S, K of PV)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
-constexpr int kEmuPairs = 3;               // of every 16 column pairs, this many use ex2_emu2
+#ifndef SECO_FWD_EMU
+#define SECO_FWD_EMU 0
+#endif
+constexpr int kEmuPairs = SECO_FWD_EMU;    // of every 16 column pairs, this many use ex2_emu2
 
 template <int NH, int D, int STAGES>
 struct Layout {
@@ -35,8 +45,8 @@ struct Layout {
   static constexpr int kQ = 0;
   static constexpr int kKV = kQ + NH * kTileBytes;
   static constexpr int kBar = kKV + STAGES * kTileBytes;
-  // barriers: q[NH], kv_full[STAGES], kv_empty[STAGES], s_full[NH], p_full[NH], o_full[NH]
-  static constexpr int kNumBars = NH + 2 * STAGES + 3 * NH;
+  // barriers: q[NH], kv_full[STAGES], kv_empty[STAGES], s_full[NH], p_half[NH][2], o_full[NH]
+  static constexpr int kNumBars = NH + 2 * STAGES + 4 * NH;
   static constexpr int kTmemSlot = kBar + 8 * kNumBars;
   static constexpr int kBytes = kTmemSlot + 16;
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-B alignment
@@ -48,7 +58,9 @@ struct Args {
   int c, j, hq, G, nqt, nhp;  // chunk size, chunk index, q heads, group size, q tiles, head packs
   float scale_log2;           // sigma * log2(e)
   int64_t qh, qr;             // o strides (elements)
+  unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters]
 };
+constexpr int kTraceCtas = 2, kTraceSlots = 12, kTraceIters = 256;
 }  // namespace fwd
 
 template <int NH, int D, int STAGES>
@@ -68,11 +80,21 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   auto bar_kv_full = [&](int s) { return bar0 + 8u * (NH + s); };
   auto bar_kv_empty = [&](int s) { return bar0 + 8u * (NH + STAGES + s); };
   auto bar_s_full = [&](int b) { return bar0 + 8u * (NH + 2 * STAGES + b); };
-  auto bar_p_full = [&](int b) { return bar0 + 8u * (2 * NH + 2 * STAGES + b); };
-  auto bar_o_full = [&](int b) { return bar0 + 8u * (3 * NH + 2 * STAGES + b); };
+  // p_half(b, 0/1): P_b for keys 0-63 / 64-127 is in TMEM (one arrival per softmax warp)
+  auto bar_p_half = [&](int b, int hf) { return bar0 + 8u * (2 * NH + 2 * STAGES + 2 * b + hf); };
+  auto bar_o_full = [&](int b) { return bar0 + 8u * (4 * NH + 2 * STAGES + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#ifdef SECO_TRACE
+#define FTRACE(slot, i)                                                                                      \
+  do {                                                                                                       \
+    if (a.trace && blockIdx.x < fwd::kTraceCtas && (i) < fwd::kTraceIters)                                   \
+      a.trace[((size_t)blockIdx.x * fwd::kTraceSlots + (slot)) * fwd::kTraceIters + (i)] = clock64();       \
+  } while (0)
+#else
+#define FTRACE(slot, i) do { } while (0)
+#endif
   // heavier query tiles first (longest-processing-time order)
   const int qt = a.nqt - 1 - (int)blockIdx.x / a.nhp;
   const int hp = (int)blockIdx.x % a.nhp;
@@ -85,7 +107,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     for (int s = 0; s < STAGES; ++s) { mbar_init(bar_kv_full(s), 1); mbar_init(bar_kv_empty(s), 1); }
     for (int b = 0; b < NH; ++b) {
       mbar_init(bar_s_full(b), 1);
-      mbar_init(bar_p_full(b), 128);
+      mbar_init(bar_p_half(b, 0), 4);
+      mbar_init(bar_p_half(b, 1), 4);
       mbar_init(bar_o_full(b), 1);
     }
     fence_barrier_init();
@@ -132,10 +155,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
                  idesc_s, kk > 0);
         }
       };
-      auto issue_pv = [&](int b, int slot, bool acc) {
+      auto issue_pv_half = [&](int b, int slot, int hf, bool acc) {   // keys [64 hf, 64 hf + 64)
         const uint32_t va = sKV + slot * L::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < fwd::BN / 16; ++kk) {
+        for (int k4 = 0; k4 < fwd::BN / 32; ++k4) {
+          const int kk = hf * (fwd::BN / 32) + k4;
           const uint64_t bd = make_desc_sw128(va + kk * 2048, BOX, 1024);
           mma_ts(tmem + NH * fwd::BN + b * D, tmem + b * fwd::BN + kk * 8, bd, idesc_pv, (acc || kk > 0) ? 1u : 0u);
         }
@@ -156,14 +180,19 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         const int kslot = slot;
         const bool more = t + 1 < T;
         for (int b = 0; b < NH; ++b) {
-          mbar_wait(bar_p_full(b), t & 1);
+          mbar_wait(bar_p_half(b, 0), t & 1);
+          FTRACE(0 + b, t);
           tc_fence_after();
-          issue_pv(b, vslot, t > 0);
+          issue_pv_half(b, vslot, 0, t > 0);
+          mbar_wait(bar_p_half(b, 1), t & 1);
+          tc_fence_after();
+          issue_pv_half(b, vslot, 1, true);
           mma_commit(bar_o_full(b));
           if (more) {
             if (b == 0) { mbar_wait(bar_kv_full(kslot), phase); tc_fence_after(); }
             issue_s(b, kslot);
             mma_commit(bar_s_full(b));
+            FTRACE(2 + b, t);
           }
         }
         mma_commit(bar_kv_empty(vslot));
@@ -186,9 +215,10 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     float m = -INFINITY, l = 0.f;
     for (int t = 0; t < T; ++t) {
       mbar_wait(bar_s_full(b), t & 1);
+      if (lane == 0 && wq == 0) FTRACE(4 + b, t);
       tc_fence_after();
       const bool diag = (t == T - 1);   // the only tile that needs the causal mask
-      // single pass: the whole 128-column row of S_b in registers (4 loads, one wait)
+      // the whole 128-column row of S_b in registers (4 loads, one wait)
       uint32_t v[fwd::BN];
 #pragma unroll
       for (int cc = 0; cc < fwd::BN / 32; ++cc) tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cc * 32));
@@ -204,51 +234,62 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         mx0 = fmax3(mx0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
         mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
       }
+      if (lane == 0 && wq == 0) FTRACE(6 + b, t);
       const float m_new = fmaxf(m, fmaxf(mx0, mx1) * sl2);
       const bool need = m_new > m + fwd::kRescaleThreshold;
       const float m_use = need ? m_new : m;
       const float alpha = need ? ex2(m - m_new) : 1.f;
       l *= alpha;
-      // P = exp2(S sigma log2e - m) -> bf16 -> TMEM columns [16cc, 16cc+16) of S_b's block
-      // (masked entries hold -inf and give exactly 0)
-      const f2_t negm = f2(-m_use, -m_use);
-      f2_t lsum0 = f2(0.f, 0.f), lsum1 = f2(0.f, 0.f);
-#pragma unroll
-      for (int cc = 0; cc < fwd::BN / 32; ++cc) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const f2_t x = ffma2(f2u(v[cc * 32 + i], v[cc * 32 + i + 1]), sl2x2, negm);
-          f2_t p2;
-          if ((i / 2) < fwd::kEmuPairs && !diag) {   // masked (-inf) entries take MUFU: exact 0
-            p2 = ex2_emu2(x);
-          } else {
-            p2 = f2(ex2(f2lo(x)), ex2(f2hi(x)));
-          }
-          if ((i / 2) & 1) lsum1 = fadd2(lsum1, p2); else lsum0 = fadd2(lsum0, p2);
-          pk[i / 2] = pack_bf16_f2(p2);
-        }
-        tmem_st16(tS + cc * 16, pk);
-      }
-      const f2_t lsum = fadd2(lsum0, lsum1);
-      l += f2lo(lsum) + f2hi(lsum);
+      // lazy O rescale: only when some row's max grew by > 2^8, and before PV_b(t) accumulates.
+      // PV_b(t-1) is complete here (S_b(t), issued after it, has completed).
       if (t > 0 && __any_sync(0xffffffffu, need)) {
-        mbar_wait(bar_o_full(b), (t - 1) & 1);  // PV_b(t-1) complete: O_b stable
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-          uint32_t v[32];
-          tmem_ld32(tO + cc * 32, v);
+#pragma unroll 1
+        for (int cc = 0; cc < D / 8; ++cc) {   // 8 columns at a time: S_b's row is live in registers
+          uint32_t ov[8];
+          tmem_ld8(tO + cc * 8, ov);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          tmem_st32(tO + cc * 32, v);
+          for (int i = 0; i < 8; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st8(tO + cc * 8, ov);
         }
       }
-      tmem_wait_st();
       m = m_use;
-      tc_fence_before();
-      mbar_arrive(bar_p_full(b));
+      // P = exp2(S sigma log2e - m) -> bf16 -> TMEM columns [16cc, 16cc+16) of S_b's block, in two
+      // halves (keys 0-63, 64-127), each released to the MMA warp as soon as it is stored, so
+      // PV on the first half overlaps the exponentials of the second.  Masked entries hold -inf
+      // and give exactly 0 through MUFU.
+      const f2_t negm = f2(-m_use, -m_use);
+      f2_t lsum0 = f2(0.f, 0.f), lsum1 = f2(0.f, 0.f);
+      auto exp_half = [&](int hf, auto emu_pairs) {
+        constexpr int EMU = decltype(emu_pairs)::value;
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const int cc = hf * 2 + c2;
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const f2_t x = ffma2(f2u(v[cc * 32 + i], v[cc * 32 + i + 1]), sl2x2, negm);
+            // EMU of the 16 pairs, evenly spread, run on the FMA pipe (ex2_emu2)
+            const bool emu = ((i / 2) * EMU) / 16 != ((i / 2 + 1) * EMU) / 16;
+            const f2_t p2 = emu ? ex2_emu2(x) : f2(ex2(f2lo(x)), ex2(f2hi(x)));
+            if ((i / 2) & 1) lsum1 = fadd2(lsum1, p2); else lsum0 = fadd2(lsum0, p2);
+            pk[i / 2] = pack_bf16_f2(p2);
+          }
+          tmem_st16(tS + cc * 16, pk);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_p_half(b, hf));
+      };
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        if (diag) exp_half(hf, std::integral_constant<int, 0>{});
+        else exp_half(hf, std::integral_constant<int, fwd::kEmuPairs>{});
+      }
+      if (lane == 0 && wq == 0) FTRACE(8 + b, t);
+      const f2_t lsum = fadd2(lsum0, lsum1);
+      l += f2lo(lsum) + f2hi(lsum);
     }
     mbar_wait(bar_o_full(b), (T - 1) & 1);
     tc_fence_after();
@@ -298,6 +339,17 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   a.nqt = g.c / fwd::BM; a.nhp = g.hq / NH;
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.qh = g.qh; a.qr = g.qr;
+  a.trace = nullptr;
+#ifdef SECO_TRACE
+  {
+    static unsigned long long* tbuf = nullptr;
+    const size_t n = (size_t)fwd::kTraceCtas * fwd::kTraceSlots * fwd::kTraceIters;
+    if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * n);
+    cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * n, st);
+    a.trace = tbuf;
+    seco_fwd_trace_buffer = tbuf;
+  }
+#endif
   dim3 grid(a.nqt * a.nhp);
   kern<<<grid, L::kThreads, L::kAlloc, st>>>(tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, a);
   return cudaGetLastError();
