@@ -185,10 +185,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     cfg = dict(CONFIGS[args.config])
     hq, hkv, d, seq, c = cfg["hq"], cfg["hkv"], cfg["d"], cfg["seq"], cfg["chunk"]
+    from paper_2505_16710_b200.parallel import head_shard, max_over_ranks
     if args.shard == "heads" and world > 1:
-        if hkv % world:
-            raise SystemExit(f"--shard heads needs Hkv % N == 0 (Hkv={hkv}, N={world})")
-        hq_r, hkv_r = hq // world, hkv // world
+        shard = head_shard(hq, hkv, world, rank)      # no collective on the data path
+        hq_r, hkv_r = shard.hq, shard.hkv
     else:
         hq_r, hkv_r = hq, hkv
     k = seq // c
@@ -262,11 +262,7 @@ def main():
                 t_f += dt
             else:
                 t_b += dt
-    ms = ms_local
-    if world > 1:
-        tt = torch.tensor([ms_local], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ms_local, dev)
     ms_per_step = ms / args.steps
 
     step_flops_rank = FL.seco_step_flops(hq_r, d, seq, c) if sel is None else \
@@ -322,11 +318,7 @@ def main():
             out_dkv.copy_(layer.dkv, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([ems], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+        ems = max_over_ranks(e0.elapsed_time(e1), dev)
         e2e = {"value": total_flops / (ems / args.steps * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": ems / args.steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "pinned host Q,K,V,dO -> device; SeCO/SpaCO step via C ABI; dQ, dKV -> pinned host"}

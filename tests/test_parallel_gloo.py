@@ -1,0 +1,64 @@
+"""N > 1 host logic on CPU (gloo, world_size 2): head sharding partitions the heads,
+needs no exchange (each rank's oracle result on its slice equals the matching slice
+of the unsharded result), and the timing reduction takes the max over ranks."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2505_16710_b200.parallel import head_shard, max_over_ranks
+
+
+def test_head_shard_partition():
+    for hq, hkv, world in ((32, 8, 1), (32, 8, 2), (32, 8, 4), (32, 8, 8), (6, 2, 2)):
+        seen_q, seen_kv = [], []
+        for r in range(world):
+            s = head_shard(hq, hkv, world, r)
+            seen_q += list(range(*s.q_heads))
+            seen_kv += list(range(*s.kv_heads))
+            G = hq // hkv
+            assert all(h // G in range(*s.kv_heads) for h in range(*s.q_heads))
+        assert seen_q == list(range(hq)) and seen_kv == list(range(hkv))
+    with pytest.raises(ValueError):
+        head_shard(32, 8, 3, 0)
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import chunkwise as OC
+        from synth import make_inputs
+        hq, hkv, S, d, c = 4, 2, 48, 8, 16
+        x = make_inputs(hq, hkv, S, d, seed=3, bf16=False)
+        s = head_shard(hq, hkv, world, rank)
+        sl_q, sl_kv = slice(*s.q_heads), slice(*s.kv_heads)
+        r = OC.seco_step(x.q[sl_q], x.k[sl_kv], x.v[sl_kv], x.do[sl_q], [c] * (S // c))
+        # gather every rank's shard of dK to rank 0 (test only; the product path has no collective)
+        dk = torch.from_numpy(r["dk"])
+        parts = [torch.zeros_like(dk) for _ in range(world)]
+        dist.all_gather(parts, dk)
+        t = max_over_ranks(10.0 + rank)
+        if rank == 0:
+            full = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (S // c))
+            out["dk_err"] = float(np.abs(torch.cat(parts).numpy() - full["dk"]).max())
+            out["tmax"] = t
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_oracle_equals_unsharded_gloo():
+    world = 2
+    port = 29500 + (os.getpid() % 1000)
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+        assert out["dk_err"] == 0.0          # bit-identical: shards share nothing
+        assert out["tmax"] == 11.0           # max over ranks
+
+
+def test_max_over_ranks_single_process():
+    assert max_over_ranks(3.5) == 3.5
