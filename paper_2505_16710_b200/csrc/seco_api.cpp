@@ -212,11 +212,11 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
   const int S_used = (j + 1) * s->chunk;
   CUtensorMap tq, tdo, tk, tv, tdq, tdkv;
   const int64_t S = (int64_t)s->chunk * s->num_chunks;
-  if (!encode_3d(&tq, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64) ||
-      !encode_3d(&tdo, d_o, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64) ||
+  if (!encode_3d(&tq, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 128) ||
+      !encode_3d(&tdo, d_o, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 128) ||
       !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
       !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
-      !encode_f32_rows(&tdq, ws_dqacc, (int64_t)s->hq * s->chunk, 64) ||
+      !encode_f32_rows(&tdq, ws_dqacc, (int64_t)s->hq * s->chunk, 128) ||
       !encode_f32_rows(&tdkv, dkv, 2 * (int64_t)s->hkv * S, 128))
     return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   e = seco::launch_bwd_sm100(g, tq, tdo, tk, tv, tdq, tdkv, o, d_o, lse, relay_scale, grad_scale, dkv, dq, dk_own, dv_own,

@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 lib = _lib.load()
 lib.seco_debug_trace_ptr.restype = ctypes.c_void_p
 ptr = lib.seco_debug_trace_ptr()
-CT, SL, IT = 4, 10, 128
+CT, SL, IT = 4, 14, 128
 host = np.zeros((CT, SL, IT), dtype=np.uint64)
 cudart = ctypes.CDLL("libcudart.so.12")
 cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
@@ -44,17 +44,18 @@ t = host.astype(np.int64)
 for cta in range(2):
     n = int((t[cta, 1] > 0).sum())
     print(f"CTA {cta}: {n} iterations")
-    base = t[cta, 1, 0]
-    rows = []
-    for i in range(1, min(n, 40)):
-        period = t[cta, 1, i] - t[cta, 1, i - 1] if i < n else 0
-        s_lat = t[cta, 5, i] - t[cta, 1, i - 1]
+    for i in range(1, min(n, 12)):
+        period = t[cta, 1, i] - t[cta, 1, i - 1]
+        kvq = t[cta, 2, i] - t[cta, 1, i]          # dV dK dQ^T issue (blocking issue)
+        dqw = t[cta, 3, i] - t[cta, 2, i] if t[cta, 3, i] else 0     # dP(i+1) issue + wait dq_empty
+        s_lat = t[cta, 5, i] - t[cta, 4, i - 1]     # S(i) issued -> compute sees s_full
         comp = t[cta, 6, i] - t[cta, 5, i]
-        comp1 = t[cta, 9, i] - t[cta, 5, i]
-        dqw = t[cta, 3, i] - t[cta, 2, i] if t[cta, 2, i] else 0
         drain = t[cta, 8, i] - t[cta, 7, i]
-        prod = t[cta, 0, i] - base if t[cta, 0, i] else 0
-        print(f"  i={i:3d} period={period:6d} s_lat={s_lat:6d} comp={comp:6d} [{comp1:6d}] dqwait={dqw:6d} "
-              f"drain={drain:6d} prod_t={prod:8d}")
+        print(f"  i={i:3d} period={period:6d} issue_kvq={kvq:6d} dP+dqwait={dqw:6d} s_lat={s_lat:6d} "
+              f"comp={comp:6d} drain={drain:6d}")
+    for i in range(2, 6):
+        b = t[cta, 5, i]
+        print(f"    compute detail i={i}: r0_ld={t[cta,10,i]-b} r0_math={t[cta,11,i]-b} r1_ld={t[cta,12,i]-b} "
+              f"r1_math={t[cta,13,i]-b} arrive={t[cta,6,i]-b}")
     per = np.diff(t[cta, 1, :n])
-    print(f"  mean period {per.mean():.0f} cycles over {n} iterations; MMA ideal 1280")
+    print(f"  mean period {per.mean():.0f} cycles over {n} iterations (128 query rows each); MMA ideal 2560")
