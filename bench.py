@@ -286,9 +286,11 @@ def main():
     except Exception:
         peak, peak_src, peak_burst = 1400.0, "fallback B200_PROFILING.md sustained ~1.4 PF", 1590.0
     traffic = None
+    traffic_launch = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
         traffic = tr.get(dom, {}).get(args.config)
+        traffic_launch = tr.get(dom, {}).get(args.config + "_launch")
     except Exception:
         pass
     achieved = kern[dom]["tflops"]
@@ -296,7 +298,9 @@ def main():
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
                 "kernel": f"seco_chunk_{'backward' if dom == 'bwd' else 'forward'} "
                           f"({'bwd_prep + seco_bwd_sm100_kernel + bwd_final' if dom == 'bwd' else 'seco_fwd_sm100_kernel'})",
-                "peak_source": peak_src, "frac_of_burst_peak": achieved / peak_burst if achieved else None}
+                "peak_source": peak_src, "frac_of_burst_peak": achieved / peak_burst if achieved else None,
+                "traffic_note": f"DRAM bytes of the {traffic_launch} launch from ncu --set full "
+                                "(profiles/roofline_traffic.json); achieved averages all launches"}
 
     # ---------------------------------------------------------------- end to end (host buffers)
     e2e = None
