@@ -77,9 +77,12 @@ size_t seco_workspace_size(const seco_shape* shape);
 /* Chunk forward (Eq. 1; Alg. 1 lines 2 and 5): for the c
  * query rows of chunk j, attend to cache slots 0..j (own slot causally) with
  * an online softmax; write O_j (o) and LSE_j (lse).  Slot j of k_cache/v_cache
- * must already hold chunk j's keys/values.  Deterministic: the stage-2 rebuild
- * reproduces stage 1 bit for bit.  `ws` may be NULL when
- * seco_workspace_size() == 0 is not required by the chosen schedule. */
+ * must already hold chunk j's keys/values.  `ws` is optional: when it is given
+ * (ws_bytes >= seco_workspace_size()), long chunks may split each query tile's
+ * key range over several CTAs (split-KV) and merge the partial results with the
+ * exact LSE-weighted combine; with ws == NULL no split is used.  Deterministic
+ * for a given (shape, j, ws != NULL): the stage-2 rebuild reproduces stage 1
+ * bit for bit. */
 seco_status seco_chunk_forward(const seco_shape* shape, int32_t j,
                                const void* q, const void* k_cache, const void* v_cache,
                                void* o, float* lse,

@@ -175,6 +175,48 @@ cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, 
                                      reinterpret_cast<__nv_bfloat16*>(dv_own), dq_scale, st);
 }
 
+// ===================================================================== split-KV combine (§8 a9)
+// O = sum_s exp(LSE_s - LSE) O_s,  LSE = log sum_s exp(LSE_s)   (exact merge of softmax partials
+// over disjoint key ranges).  One warp per (head, row); each lane owns 4 of the d = 128 columns.
+struct CombArgs {
+  int hq, c, nsplit;
+  int64_t qh, qr;
+};
+__global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restrict__ part_o,
+                                                          const float* __restrict__ part_lse,
+                                                          __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
+                                                          CombArgs a) {
+  const int w = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (w >= a.hq * a.c) return;
+  const int h = w / a.c, r = w % a.c;
+  const int64_t plane = (int64_t)a.hq * a.c;
+  float mx = -INFINITY;
+  for (int s = 0; s < a.nsplit; ++s) mx = fmaxf(mx, part_lse[s * plane + w]);
+  float den = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < a.nsplit; ++s) {
+    const float wt = __expf(part_lse[s * plane + w] - mx);
+    den += wt;
+    const float4 v = reinterpret_cast<const float4*>(part_o + (s * plane + w) * 128)[lane];
+    acc.x += wt * v.x; acc.y += wt * v.y; acc.z += wt * v.z; acc.w += wt * v.w;
+  }
+  const float inv = 1.f / den;
+  uint2 pk;
+  pk.x = pack_bf16(acc.x * inv, acc.y * inv);
+  pk.y = pack_bf16(acc.z * inv, acc.w * inv);
+  *reinterpret_cast<uint2*>(o + (int64_t)h * a.qh + (int64_t)r * a.qr + 4 * lane) = pk;
+  if (lane == 0) lse[w] = mx + __logf(den);
+}
+
+cudaError_t launch_fwd_combine(const ChunkGeom& g, int nsplit, const float* part_o, const float* part_lse, void* o,
+                               float* lse, cudaStream_t st) {
+  CombArgs a;
+  a.hq = g.hq; a.c = g.c; a.nsplit = nsplit; a.qh = g.qh; a.qr = g.qr;
+  fwd_combine_kernel<<<(g.hq * g.c + 7) / 8, 256, 0, st>>>(part_o, part_lse, reinterpret_cast<__nv_bfloat16*>(o),
+                                                            lse, a);
+  return cudaGetLastError();
+}
+
 // ===================================================================== fp32 debug path
 struct DbgArgs {
   int hq, hkv, G, c, d, j;

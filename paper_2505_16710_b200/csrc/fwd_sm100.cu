@@ -37,7 +37,8 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when th
 #ifndef SECO_FWD_EMU
 #define SECO_FWD_EMU 0
 #endif
-constexpr int kEmuPairs = SECO_FWD_EMU;    // of every 16 column pairs, this many use ex2_emu2
+constexpr int kEmuPairs = SECO_FWD_EMU;
+constexpr int kSMs = 148;                  // B200    // of every 16 column pairs, this many use ex2_emu2
 
 template <int NH, int D, int STAGES>
 struct Layout {
@@ -56,8 +57,11 @@ struct Layout {
 
 struct Args {
   int c, j, hq, G, nqt, nhp;  // chunk size, chunk index, q heads, group size, q tiles, head packs
+  int nsplit;                 // split-KV factor (1: final O/LSE written directly)
   float scale_log2;           // sigma * log2(e)
   int64_t qh, qr;             // o strides (elements)
+  float* part_o;              // nsplit > 1: [nsplit][hq][c][D] fp32 normalised partial O
+  float* part_lse;            // nsplit > 1: [nsplit][hq][c] partial LSE (natural log)
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters]
 };
 constexpr int kTraceCtas = 2, kTraceSlots = 12, kTraceIters = 256;
@@ -95,12 +99,15 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
 #else
 #define FTRACE(slot, i) do { } while (0)
 #endif
-  // heavier query tiles first (longest-processing-time order)
-  const int qt = a.nqt - 1 - (int)blockIdx.x / a.nhp;
-  const int hp = (int)blockIdx.x % a.nhp;
+  // heavier query tiles first (longest-processing-time order); split-KV part innermost
+  const int unit = (int)blockIdx.x / a.nsplit, split = (int)blockIdx.x % a.nsplit;
+  const int qt = a.nqt - 1 - unit / a.nhp;
+  const int hp = unit % a.nhp;
   const int h0 = hp * NH, g = h0 / a.G;
   const int q0 = a.j * a.c + qt * fwd::BM;  // absolute position of the tile's first row
   const int T = q0 / fwd::BN + 1;           // K/V tiles 0..T-1; tile T-1 is the causal diagonal
+  const int t0 = T * split / a.nsplit;      // this CTA's K/V tiles: [t0, t0 + nT)
+  const int nT = T * (split + 1) / a.nsplit - t0;
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < NH; ++b) mbar_init(bar_q(b), 1);
@@ -130,7 +137,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       }
       int slot = 0;
       uint32_t phase = 0;
-      for (int t = 0; t < T; ++t) {
+      for (int t = t0; t < t0 + nT; ++t) {
         for (int w = 0; w < 2; ++w) {  // K_t then V_t
           mbar_wait(bar_kv_empty(slot), phase ^ 1);
           mbar_expect_tx(bar_kv_full(slot), L::kTileBytes);
@@ -173,12 +180,12 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       for (int b = 0; b < NH; ++b) { issue_s(b, slot); mma_commit(bar_s_full(b)); }
       mma_commit(bar_kv_empty(slot));
       if (++slot == STAGES) { slot = 0; phase ^= 1; }
-      for (int t = 0; t < T; ++t) {
+      for (int t = 0; t < nT; ++t) {   // t counts this CTA's tiles
         const int vslot = slot;
         mbar_wait(bar_kv_full(vslot), phase);
         if (++slot == STAGES) { slot = 0; phase ^= 1; }
         const int kslot = slot;
-        const bool more = t + 1 < T;
+        const bool more = t + 1 < nT;
         for (int b = 0; b < NH; ++b) {
           mbar_wait(bar_p_half(b, 0), t & 1);
           FTRACE(0 + b, t);
@@ -213,11 +220,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     const float sl2 = a.scale_log2;
     const f2_t sl2x2 = f2(sl2, sl2);
     float m = -INFINITY, l = 0.f;
-    for (int t = 0; t < T; ++t) {
+    for (int t = 0; t < nT; ++t) {   // t counts this CTA's tiles; global tile index t0 + t
       mbar_wait(bar_s_full(b), t & 1);
       if (lane == 0 && wq == 0) FTRACE(4 + b, t);
       tc_fence_after();
-      const bool diag = (t == T - 1);   // the only tile that needs the causal mask
+      const bool diag = (t0 + t == T - 1);   // the only tile that needs the causal mask
       // the whole 128-column row of S_b in registers (4 loads, one wait)
       uint32_t v[fwd::BN];
 #pragma unroll
@@ -291,29 +298,47 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       const f2_t lsum = fadd2(lsum0, lsum1);
       l += f2lo(lsum) + f2hi(lsum);
     }
-    mbar_wait(bar_o_full(b), (T - 1) & 1);
+    mbar_wait(bar_o_full(b), (nT - 1) & 1);
     tc_fence_after();
-    // epilogue: O = acc / l (bf16), LSE = (m + log2 l) ln 2
+    // epilogue: O = acc / l, LSE = (m + log2 l) ln 2 -- bf16 O directly, or (split-KV) the
+    // normalised fp32 partial for the combine kernel
     const int h = h0 + b;
     const float inv_l = 1.f / l;
-    __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)(qt * fwd::BM + r) * a.qr;
+    const float lse_v = (m + __log2f(l)) * 0.69314718055994531f;
+    if (a.nsplit == 1) {
+      __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)(qt * fwd::BM + r) * a.qr;
 #pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t v[32];
-      tmem_ld32(tO + cc * 32, v);
-      tmem_wait_ld();
-      uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tO + cc * 32, v);
+        tmem_wait_ld();
+        uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(v[8 * q + 0]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l);
-        w.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l);
-        w.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l);
-        w.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l);
-        dst[q] = w;
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(v[8 * q + 0]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l);
+          w.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l);
+          w.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l);
+          w.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l);
+          dst[q] = w;
+        }
       }
+      lse[(int64_t)h * a.c + qt * fwd::BM + r] = lse_v;
+    } else {
+      const int64_t prow = ((int64_t)split * a.hq + h) * a.c + qt * fwd::BM + r;
+      float4* dst = reinterpret_cast<float4*>(a.part_o + prow * D);
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tO + cc * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          dst[cc * 8 + q] = make_float4(__uint_as_float(v[4 * q]) * inv_l, __uint_as_float(v[4 * q + 1]) * inv_l,
+                                        __uint_as_float(v[4 * q + 2]) * inv_l, __uint_as_float(v[4 * q + 3]) * inv_l);
+      }
+      a.part_lse[prow] = lse_v;
     }
-    lse[(int64_t)h * a.c + qt * fwd::BM + r] = (m + __log2f(l)) * 0.69314718055994531f;
   }
   __syncwarp();
   tc_fence_before();
@@ -322,9 +347,13 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   if (warp == 2) tmem_dealloc<L::kTmemCols>(tmem);
 }
 
+cudaError_t launch_fwd_combine(const ChunkGeom& g, int nsplit, const float* part_o, const float* part_lse, void* o,
+                               float* lse, cudaStream_t st);
+
 template <int NH, int D, int STAGES>
 static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
-                                   const CUtensorMap& tv, void* o, float* lse, cudaStream_t st) {
+                                   const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
+                                   cudaStream_t st, int* launches) {
   using L = fwd::Layout<NH, D, STAGES>;
   static_assert(L::kAlloc <= 232448, "shared memory budget");
   auto kern = seco_fwd_sm100_kernel<NH, D, STAGES>;
@@ -339,6 +368,26 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   a.nqt = g.c / fwd::BM; a.nhp = g.hq / NH;
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.qh = g.qh; a.qr = g.qr;
+  // split-KV (§8 row a9) when the chunk has too few equal-cost units (q tiles x head packs)
+  // to fill the SMs -- e.g. head-sharded ranks.  Cost model in K/V-tile units per wave:
+  // ~8 tiles of prologue/epilogue per work item, 15% of a unit for the fp32 partial
+  // write + combine; measured on B200: a 2-wave grid (cfg3, 256 units) is NOT worth
+  // splitting, a sub-wave grid is.
+  const int units = a.nqt * a.nhp;
+  const int t_min = g.j * g.c / fwd::BN + 1;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int sp = 1; sp <= 4; ++sp) {
+    if (sp > 1 && (t_min < 8 * sp || g.j == 0 || ws == nullptr ||
+                   (size_t)sp * g.hq * g.c * (D + 1) > ws_floats))
+      break;
+    const double waves = (double)((units * sp + fwd::kSMs - 1) / fwd::kSMs);
+    const double cost = waves * ((double)t_min / sp + 8.0) + (sp > 1 ? 0.15 * t_min : 0.0);
+    if (cost < best_cost) { best_cost = cost; best = sp; }
+  }
+  a.nsplit = best;
+  a.part_o = ws;
+  a.part_lse = ws ? ws + (size_t)best * g.hq * g.c * D : nullptr;
   a.trace = nullptr;
 #ifdef SECO_TRACE
   {
@@ -350,17 +399,24 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
     seco_fwd_trace_buffer = tbuf;
   }
 #endif
-  dim3 grid(a.nqt * a.nhp);
+  dim3 grid(units * a.nsplit);
   kern<<<grid, L::kThreads, L::kAlloc, st>>>(tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, a);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  *launches = 1;
+  if (e == cudaSuccess && a.nsplit > 1) {
+    e = launch_fwd_combine(g, a.nsplit, a.part_o, a.part_lse, o, lse, st);
+    *launches = 2;
+  }
+  return e;
 }
 
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, void* o, float* lse, cudaStream_t st) {
+                             const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
+                             cudaStream_t st, int* launches) {
   const int G = g.hq / g.hkv;
   if (g.d == 128) {
-    if (G % 2 == 0) return launch_fwd_impl<2, 128, 5>(g, tq, tk, tv, o, lse, st);
-    return launch_fwd_impl<1, 128, 6>(g, tq, tk, tv, o, lse, st);
+    if (G % 2 == 0) return launch_fwd_impl<2, 128, 5>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
+    return launch_fwd_impl<1, 128, 6>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
   }
   return cudaErrorInvalidValue;
 }

@@ -24,7 +24,8 @@ cudaError_t launch_bwd_fp32(const ChunkGeom& g, const float* q, const float* k, 
 
 // ---- bf16 tensor-core path (tcgen05 / TMEM / TMA) -----------------------------------
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, void* o, float* lse, cudaStream_t st);
+                             const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
+                             cudaStream_t st, int* launches);
 cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tdo,
                              const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tdq,
                              const CUtensorMap& tdkv, const void* o, const void* d_o,

@@ -113,8 +113,11 @@ seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
 }
 
 size_t ws_floats(const seco_shape* s) {
-  // dQ accumulator [hq][c][d] + D [hq][c] + (-LSE log2 e) [hq][c]
-  return (size_t)s->hq * s->chunk * s->d + 2 * (size_t)s->hq * s->chunk;
+  // backward: dQ accumulator [hq][c][d] + D [hq][c] + (-LSE log2 e) [hq][c]
+  // forward (split-KV, up to 4 parts): partial O [4][hq][c][d] + partial LSE [4][hq][c]
+  const size_t bwd = (size_t)s->hq * s->chunk * s->d + 2 * (size_t)s->hq * s->chunk;
+  const size_t fwd = 4 * (size_t)s->hq * s->chunk * (s->d + 1);
+  return bwd > fwd ? bwd : fwd;
 }
 
 // ---- splitmix64 (Steele, Lea & Flood 2014), state = seed
@@ -153,7 +156,6 @@ size_t seco_workspace_size(const seco_shape* s) {
 
 seco_status seco_chunk_forward(const seco_shape* s, int32_t j, const void* q, const void* k, const void* v, void* o,
                                float* lse, void* ws, size_t ws_bytes, seco_stream_t stream) {
-  (void)ws; (void)ws_bytes;
   g_launches = 0;
   seco_status st = check_shape(s, j);
   if (st != SECO_OK) return st;
@@ -175,9 +177,12 @@ seco_status seco_chunk_forward(const seco_shape* s, int32_t j, const void* q, co
       !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
       !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128))
     return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  e = seco::launch_fwd_sm100(g, tq, tk, tv, o, lse, cs);
+  if (ws && !aligned16(ws)) return fail(SECO_ERR_ARG, "ws must be 16-byte aligned");
+  int launches = 0;
+  e = seco::launch_fwd_sm100(g, tq, tk, tv, o, lse, reinterpret_cast<float*>(ws), ws ? ws_bytes / 4 : 0, cs,
+                             &launches);
   if (e != cudaSuccess) return cuda_fail(e, "fwd_sm100");
-  g_launches = 1;
+  g_launches = launches;
   return SECO_OK;
 }
 
