@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--shard", default="heads", choices=["heads", "batch"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--allreduce", action="store_true",
+                    help="batch mode: all_reduce a LLaMA3-8B LoRA r=8 fp32 gradient bucket (27.3 MB) each step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no timing output")
@@ -185,7 +187,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     cfg = dict(CONFIGS[args.config])
     hq, hkv, d, seq, c = cfg["hq"], cfg["hkv"], cfg["d"], cfg["seq"], cfg["chunk"]
-    from paper_2505_16710_b200.parallel import head_shard, max_over_ranks
+    from paper_2505_16710_b200.parallel import (LORA_PARAMS_LLAMA3_8B_R8, allreduce_grad_bucket, head_shard,
+                                                max_over_ranks)
     if args.shard == "heads" and world > 1:
         shard = head_shard(hq, hkv, world, rank)      # no collective on the data path
         hq_r, hkv_r = shard.hq, shard.hkv
@@ -210,6 +213,7 @@ def main():
         return ops.spaco_sample_and_scale(k, args.t, args.seed, args.cap, ops._lib.SPACO_PAPER)
 
     sel, gamma, sscale = sampled()
+    bucket = torch.zeros(LORA_PARAMS_LLAMA3_8B_R8, dtype=torch.float32, device=dev) if args.allreduce else None
 
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -249,6 +253,8 @@ def main():
                 else:
                     launches += layer.backward_chunk(q, kc, vc, do, j, gamma, sscale)
                 ev[s][2 * n + 1].record(stream)
+            if bucket is not None:
+                allreduce_grad_bucket(bucket)
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -345,6 +351,7 @@ def main():
                        "hq": hq, "hkv": hkv, "d": d, "seq_len": seq, "chunk": c, "num_chunks": k,
                        "mode": args.mode, "sequences_per_step": n_seq,
                        "parallelism": f"{args.shard}{world}" if world > 1 else "single",
+                       "allreduce_bytes_per_step": (LORA_PARAMS_LLAMA3_8B_R8 * 4 if args.allreduce else 0),
                        "l2_policy": "inputs larger than L2 (Q,dO 256 MiB, K,V 64 MiB each, dKV 256 MiB per rank)"},
             "tokens_per_s": tokens / (ms_per_step * 1e-3),
             "step_tflop": total_flops / 1e12,

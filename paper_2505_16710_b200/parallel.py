@@ -51,3 +51,19 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+# LLaMA3-8B, LoRA r = 8 on the q, k, v, o projections of 32 layers: per layer
+# q: 8*(4096+4096), k: 8*(4096+1024), v: 8*(4096+1024), o: 8*(4096+4096) parameters.
+LORA_PARAMS_LLAMA3_8B_R8 = 32 * 8 * ((4096 + 4096) + 2 * (4096 + 1024) + (4096 + 4096))
+
+
+def allreduce_grad_bucket(bucket):
+    """Batch-of-sequences mode (BASELINE configs[4]): every rank ran the chunked step on
+    its own sequence; the per-rank fp32 LoRA-gradient bucket is summed over ranks with
+    one all_reduce (NCCL over NVLink on the GPU box, gloo in the CPU tests).  The only
+    device-to-device exchange of the method; a no-op on one rank."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(bucket, op=dist.ReduceOp.SUM)
+    return bucket

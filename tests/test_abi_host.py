@@ -23,7 +23,8 @@ def lib():
 
 
 def _declared_functions():
-    src = open(os.path.join(ROOT, "include", "seco.h")).read()
+    with open(os.path.join(ROOT, "include", "seco.h")) as f:
+        src = f.read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(seco_\w+|spaco_\w+)\s*\(", src)))
 
@@ -61,7 +62,9 @@ def test_sampler_bit_exact_vs_oracle(lib, mode):
 
 def test_sampler_kats_golden(lib):
     path = os.path.join(ROOT, "tests", "golden", "sampler_kats.txt")
-    for ln in open(path):
+    with open(path) as f:
+        lines = f.readlines()
+    for ln in lines:
         if not ln.strip() or ln.startswith("#"):
             continue
         mode, k, t, seed, want = ln.split()

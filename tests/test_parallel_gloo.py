@@ -9,7 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2505_16710_b200.parallel import head_shard, max_over_ranks
+from paper_2505_16710_b200.parallel import (LORA_PARAMS_LLAMA3_8B_R8, allreduce_grad_bucket, head_shard,
+                                            max_over_ranks)
 
 
 def test_head_shard_partition():
@@ -42,10 +43,13 @@ def _worker(rank, world, port, out):
         parts = [torch.zeros_like(dk) for _ in range(world)]
         dist.all_gather(parts, dk)
         t = max_over_ranks(10.0 + rank)
+        bucket = torch.full((1000,), float(rank + 1))
+        allreduce_grad_bucket(bucket)
         if rank == 0:
             full = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (S // c))
             out["dk_err"] = float(np.abs(torch.cat(parts).numpy() - full["dk"]).max())
             out["tmax"] = t
+            out["bucket"] = float(bucket[0])
     finally:
         dist.destroy_process_group()
 
@@ -53,12 +57,20 @@ def _worker(rank, world, port, out):
 def test_sharded_oracle_equals_unsharded_gloo():
     world = 2
     port = 29500 + (os.getpid() % 1000)
-    with mp.Manager() as m:
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as m:
         out = m.dict()
-        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
         assert out["dk_err"] == 0.0          # bit-identical: shards share nothing
         assert out["tmax"] == 11.0           # max over ranks
+        assert out["bucket"] == 3.0          # batch-mode gradient bucket summed over ranks
 
 
 def test_max_over_ranks_single_process():
     assert max_over_ranks(3.5) == 3.5
+
+
+def test_lora_bucket_size():
+    """LLaMA3-8B, r=8 on q,k,v,o x 32 layers = 6.82 M params = 27.3 MB fp32."""
+    assert LORA_PARAMS_LLAMA3_8B_R8 == 6_815_744
+    assert abs(LORA_PARAMS_LLAMA3_8B_R8 * 4 / 1e6 - 27.3) < 0.05
