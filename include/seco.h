@@ -22,6 +22,9 @@
  *
  * Layouts (all row-major, innermost dimension d contiguous, strides in ELEMENTS):
  *   q, o, d_o, dq : [hq][c][d]   element (h, r, x) at h*q_head_stride + r*q_row_stride + x
+ *                  (heads outermost, or rows outermost with heads interleaved, i.e.
+ *                  the [c][hq][d] output of a projection: q_head_stride = d,
+ *                  q_row_stride = hq*d; the same two choices for the KV cache)
  *   k_cache, v_cache : [hkv][S][d], S = c*num_chunks, element (g, q, x) at
  *                  g*kv_head_stride + q*kv_row_stride + x; slot j = rows [j*c, (j+1)*c)
  *   lse           : [hq][c] float32, dense
@@ -40,7 +43,7 @@
  * validated on the host before any launch (SECO_ERR_ARG: null pointer, j out of
  * range, hq % hkv != 0, non-positive sizes, misaligned pointer or stride;
  * SECO_ERR_UNSUPPORTED: a shape the bf16 tensor-core path does not implement --
- * it needs d in {64, 128}, c % 128 == 0, 16-byte aligned rows; the fp32 debug
+ * it needs d = 128, c % 128 == 0, 16-byte aligned rows; the fp32 debug
  * path accepts any d <= 256 and any c).  Launch failures return SECO_ERR_CUDA;
  * faults during execution surface at the caller's next synchronisation.
  */

@@ -80,6 +80,15 @@ bool encode_f32_rows(CUtensorMap* m, const void* ptr, int64_t rows, int box_rows
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Rows of d elements, `rows` per head, `heads` heads never share an element when either
+// heads are outermost ([h][r][d]: rs >= d, hs >= rows*rs) or rows are outermost with the
+// heads interleaved inside a row ([r][h][d], e.g. a QKV projection output: hs >= d,
+// rs >= heads*hs).
+bool disjoint(int64_t d, int64_t rows, int64_t heads, int64_t rs, int64_t hs) {
+  if (rs >= d && hs >= rows * rs) return true;
+  return hs >= d && rs >= heads * hs;
+}
+
 seco_status check_shape(const seco_shape* s, int32_t j) {
   if (!s) return fail(SECO_ERR_ARG, "shape is NULL");
   if (s->hq <= 0 || s->hkv <= 0 || s->d <= 0 || s->chunk <= 0 || s->num_chunks <= 0)
@@ -87,9 +96,9 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
                 s->num_chunks);
   if (s->hq % s->hkv) return fail(SECO_ERR_ARG, "hq %% hkv != 0 (hq=%d hkv=%d)", s->hq, s->hkv);
   if (j < 0 || j >= s->num_chunks) return fail(SECO_ERR_ARG, "chunk index j=%d out of [0,%d)", j, s->num_chunks);
-  if (s->q_row_stride < s->d || s->kv_row_stride < s->d || s->q_head_stride < (int64_t)s->chunk * s->q_row_stride ||
-      s->kv_head_stride < (int64_t)s->chunk * s->num_chunks * s->kv_row_stride)
-    return fail(SECO_ERR_ARG, "strides overlap rows/heads");
+  if (!disjoint(s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride) ||
+      !disjoint(s->d, (int64_t)s->chunk * s->num_chunks, s->hkv, s->kv_row_stride, s->kv_head_stride))
+    return fail(SECO_ERR_ARG, "strides overlap rows/heads (need head-major or row-major-interleaved rows)");
   if (s->dtype == SECO_BF16) {
     if (s->d != 128) return fail(SECO_ERR_UNSUPPORTED, "bf16 path implements d=128 (got %d)", s->d);
     if (s->chunk % 128) return fail(SECO_ERR_UNSUPPORTED, "bf16 path needs chunk %% 128 == 0 (got %d)", s->chunk);

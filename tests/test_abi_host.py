@@ -97,6 +97,9 @@ def _shape(**kw):
     (dict(dtype=1, d=300, q_row_stride=300, kv_row_stride=300, q_head_stride=1024 * 300,
           kv_head_stride=1024 * 300), 0, _lib.SECO_ERR_UNSUPPORTED),
     (dict(dtype=5), 0, _lib.SECO_ERR_ARG),
+    (dict(q_head_stride=128 * 128), 0, _lib.SECO_ERR_ARG),                  # heads overlap rows
+    (dict(q_head_stride=128, q_row_stride=16 * 128), 0, _lib.SECO_ERR_ARG),  # interleaved, too few heads/row
+    (dict(kv_head_stride=256 * 128), 0, _lib.SECO_ERR_ARG),                 # cache heads overlap
 ])
 def test_argument_validation(lib, kw, j, code):
     s = _shape(**kw)
@@ -138,3 +141,16 @@ def test_flops_pairs_brute_force():
     assert abs(flops.seco_step_flops(hq, d, S, c) / F - 4.5) < 1e-12
     assert abs(F - 8.796e12) / 8.796e12 < 1e-3     # cfg3 F = 8.796 TF
     assert flops.spaco_step_flops(hq, d, S, c, range(16)) == flops.seco_step_flops(hq, d, S, c)
+
+
+def test_workspace_independent_of_sequence_length(lib):
+    """SeCO's memory claim at this level ('reduces the memory requirements for
+    storing forward activations by a factor of k'): the per-call working set of the chunk
+    kernels depends on the chunk size c, not on the number of chunks k."""
+    sizes = set()
+    for k in (1, 4, 16, 64):
+        s = _shape(num_chunks=k, q_head_stride=k * 256 * 128, kv_head_stride=k * 256 * 128)
+        sizes.add(lib.seco_workspace_size(ctypes.byref(s)))
+    assert len(sizes) == 1
+    s2 = _shape(chunk=512, q_head_stride=4 * 512 * 128, kv_head_stride=4 * 512 * 128)
+    assert lib.seco_workspace_size(ctypes.byref(s2)) == 2 * sizes.pop()

@@ -158,3 +158,36 @@ def test_bf16_forward_split_kv(j):
     layer.forward_chunk(q, k, v, j)
     torch.cuda.synchronize()
     assert torch.equal(o1.view(torch.int16), layer.o[:, j * c:(j + 1) * c].view(torch.int16))
+
+
+def test_bf16_strided_sequence_major_layout():
+    """The ABI takes arbitrary head/row strides: Q, O, dO, dQ as [S][Hq][d] (projection output
+    layout) and the KV cache as [S][Hkv][d], passed as strided views -- same results."""
+    from paper_2505_16710_b200 import ops
+    hq, hkv, seq, d, c = 8, 2, 512, 128, 128
+    x = inputs(hq, hkv, seq, d, seed=8)
+    q, k, v, do = upload(x, torch.bfloat16)
+    qs, dos = q.transpose(0, 1).contiguous(), do.transpose(0, 1).contiguous()    # [S][H][d]
+    ks, vs = k.transpose(0, 1).contiguous(), v.transpose(0, 1).contiguous()
+    qv, dov, kv_, vv = qs.transpose(0, 1), dos.transpose(0, 1), ks.transpose(0, 1), vs.transpose(0, 1)
+    shape = ops.make_shape(qv, kv_, c)
+    assert shape.q_row_stride == hq * d and shape.q_head_stride == d
+    o = torch.empty(seq, hq, d, dtype=torch.bfloat16, device="cuda").transpose(0, 1)
+    dq = torch.zeros(seq, hq, d, dtype=torch.bfloat16, device="cuda").transpose(0, 1)
+    lse = torch.empty(seq // c, hq, c, dtype=torch.float32, device="cuda")
+    dkv = torch.zeros(2, hkv, seq, d, dtype=torch.float32, device="cuda")
+    ws = torch.empty(ops.seco_workspace_size(shape) // 4, dtype=torch.float32, device="cuda")
+    k_chunks = seq // c
+    for j in range(k_chunks):
+        ops.seco_chunk_forward(shape, j, ops.chunk_view(qv, shape, j), kv_, vv, ops.chunk_view(o, shape, j), lse[j], ws)
+    for j in reversed(range(k_chunks)):
+        ops.seco_chunk_forward(shape, j, ops.chunk_view(qv, shape, j), kv_, vv, ops.chunk_view(o, shape, j), lse[j], ws)
+        ops.seco_chunk_backward(shape, j, ops.chunk_view(qv, shape, j), kv_, vv, ops.chunk_view(o, shape, j),
+                                ops.chunk_view(dov, shape, j), lse[j], 1.0, 1.0, dkv, ops.chunk_view(dq, shape, j),
+                                None, None, ws)
+    torch.cuda.synchronize()
+    ref = OC.seco_step(x.q, x.k, x.v, x.do, [c] * k_chunks)
+    assert err(host(o), ref["o"]) <= BF16_TOL
+    assert err(host(dq), ref["dq"]) <= BF16_TOL
+    assert err(host(dkv[0]), ref["dk"]) <= BF16_TOL
+    assert err(host(dkv[1]), ref["dv"]) <= BF16_TOL
