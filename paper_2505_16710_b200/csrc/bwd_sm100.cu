@@ -18,11 +18,15 @@
 // TMEM columns: R0 [0,128)  R1 [128,256)  dK [256,384)  dV [384,512).
 // MMA issue order per tile i: dV(i) dK(i) dQ^T(i) dP(i+1) [R0 drained] S(i+1).
 // Warp roles: w0 TMA producer (K,V once; Q,dO double-buffered, LSE/D with Q), w1 MMA
-// issuer, w2 TMEM allocator, w4-w11 two compute warpgroups (thread = key row; WG w owns
-// query columns [64w, 64w+64), in two rounds of 32; between tiles the same warps read
-// dQ^T out of R0 and stage it), w12 lane 0 issues the dQ TMA reduce-adds.
+// issuer, w2 TMEM allocator, w3 lane 0 issues the dQ TMA reduce-adds, w4-w19 four compute
+// warpgroups (thread = key row; WG w owns query columns [16w, 16w+16) of each 64-column
+// half -- four warps per SM sub-partition hide the MUFU / TMEM latencies; between tiles the
+// same warps read dQ^T out of R0 and stage it).
 // The dQ staging tile (64 KiB fp32) borrows the current Q and dO buffers, both dead once
-// dQ^T(i) has started (dK(i), dV(i) consumed them); their next loads wait for the drain.  dK/dV leave TMEM once per CTA, scaled (s sigma,
+// dQ^T(i) has started (dK(i), dV(i) consumed them); their next loads wait for the drain
+// (measured: one SM drains reduce-adds at 25.6 B/clk, so the 64 KiB take ~2600 cycles, as
+// long as the tile's MMAs), the dO half first since dP^T(i+2) is issued before S^T(i+2).
+// dK/dV leave TMEM once per CTA, scaled (s sigma,
 // s), through swizzled smem staging and TMA reduce-add into dkv; slot j of dkv was
 // pre-scaled by the relay factor gamma in bwd_prep (grad_hook).
 // All fp32 reductions are issued by the TMA unit: no per-element atomics.
@@ -58,12 +62,14 @@ constexpr int kBar = kStats + 2 * 2 * BQ * 4;
 constexpr int kNumBars = 1 + 8 + 9;
 constexpr int kTmemSlot = kBar + 8 * kNumBars;
 constexpr int kBytes = kTmemSlot + 16;
-constexpr int kThreads = 512;
+constexpr int kThreads = 640;   // 4 role warps + 4 compute warpgroups
+constexpr int kWG = 4;          // compute warpgroups; WG w owns query columns {16w + 64hf}
 constexpr int R0 = 0, R1 = 128, TM_DK = 256, TM_DV = 384;
 #ifndef SECO_BWD_EMU
 #define SECO_BWD_EMU 0
 #endif
-constexpr int kEmuPairs = SECO_BWD_EMU;   // of every 16 column pairs, this many use ex2_emu2 (FMA pipe)
+constexpr int kEmuPairs = SECO_BWD_EMU;
+   // of every 16 column pairs, this many use ex2_emu2 (FMA pipe)
 
 struct Args {
   int c, j, G, hkv, S;
@@ -77,7 +83,7 @@ struct Args {
   int* err;           // set to 1 if the dynamic smem window is not 1024-B aligned
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters] clock64
 };
-constexpr int kTraceCtas = 4, kTraceSlots = 14, kTraceIters = 128;
+constexpr int kTraceCtas = 4, kTraceSlots = 20, kTraceIters = 128;
 }  // namespace bwd
 
 __global__ void __launch_bounds__(bwd::kThreads, 1)
@@ -153,12 +159,12 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       mbar_init(bar_do_empty(s), 2);    // dV has consumed dO, and the dQ drain is done with it
     }
     mbar_init(bar_s_full, 1);
-    mbar_init(bar_ds_half(0), 8);       // one elected lane per compute warp
-    mbar_init(bar_ds_half(1), 8);
+    mbar_init(bar_ds_half(0), 4 * kWG);  // one elected lane per compute warp
+    mbar_init(bar_ds_half(1), 4 * kWG);
     mbar_init(bar_dq_full, 1);
-    mbar_init(bar_dq_empty, 8);         // one elected lane per compute warp (they read R0 out)
-    mbar_init(bar_stg_half(0), 4);
-    mbar_init(bar_stg_half(1), 4);
+    mbar_init(bar_dq_empty, 4 * kWG);   // one elected lane per compute warp (they read R0 out)
+    mbar_init(bar_stg_half(0), 2 * 4);  // the 8 warps staging dQ rows [64h, 64h + 64)
+    mbar_init(bar_stg_half(1), 2 * 4);
     mbar_init(bar_acc, 1);
     mbar_init(bar_drain_done, 1);
     fence_barrier_init();
@@ -187,6 +193,11 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           const int st = i & 1;
           const uint32_t ph = (i >> 1) & 1;
           const int h = g * a.G + w.hh, qt = w.qt;
+          // dO first: dP^T(i) is issued before S^T(i), and its buffer frees earlier (dV(i-2))
+          mbar_wait(bar_do_empty(st), ph ^ 1);
+          mbar_expect_tx(bar_do_full(st), kTile);
+          for (int x = 0; x < D / 64; ++x)
+            tma_load_3d(dobuf(st) + x * kBox, &tm_do, bar_do_full(st), x * 64, qt * BQ, h);
           mbar_wait(bar_q_empty(st), ph ^ 1);
           mbar_expect_tx(bar_q_full(st), kTile + 2 * BQ * 4);
           for (int x = 0; x < D / 64; ++x)
@@ -194,10 +205,6 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           const int64_t ro = (int64_t)h * a.c + qt * BQ;
           bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_q_full(st));
           bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_q_full(st));
-          mbar_wait(bar_do_empty(st), ph ^ 1);
-          mbar_expect_tx(bar_do_full(st), kTile);
-          for (int x = 0; x < D / 64; ++x)
-            tma_load_3d(dobuf(st) + x * kBox, &tm_do, bar_do_full(st), x * 64, qt * BQ, h);
           TRACE(0, i);
         }
       }
@@ -216,12 +223,13 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           }
         };
         // A operand (P^T or dS^T, bf16 in TMEM): query k-step kk (queries 16kk..16kk+15) lives
-        // in columns base + 32(kk/2) + 8(kk%2); query half hf = k-steps 4hf .. 4hf+3
+        // packed in columns base + 16kk .. +7 (over the S^T / dP^T columns of those queries, which
+        // their compute warp has already read); query half hf = k-steps 4hf .. 4hf+3
         auto issue_kv = [&](uint32_t a_col, uint32_t b_base, uint32_t d_col, int hf, bool acc) {
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int kk = 4 * hf + k4;
-            mma_ts(tmem + d_col, tmem + a_col + 32 * (kk / 2) + 8 * (kk % 2),
+            mma_ts(tmem + d_col, tmem + a_col + 16 * kk,
                    make_desc_sw128(b_base + kk * 2048, kBox, 1024), idesc_kv, (acc || kk > 0) ? 1u : 0u);
           }
         };
@@ -241,6 +249,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           issue_kv(R0, dobuf(st), TM_DV, 0, i > 0);
           issue_kv(R1, qbuf(st), TM_DK, 0, i > 0);
           mbar_wait(bar_ds_half(1), i & 1);
+          TRACE(16, i);
           tc_fence_after();
           issue_kv(R0, dobuf(st), TM_DV, 1, true);
           mma_commit(bar_do_empty(st));
@@ -258,6 +267,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
             mbar_wait(bar_do_full(st1), ph1);
             tc_fence_after();
             issue_sdp(sV, dobuf(st1), R1);                  // dP^T(i+1) -> R1 (dS^T(i) consumed by dK(i))
+            TRACE(17, i);
             mbar_wait(bar_dq_empty, i & 1);                 // R0 drained
             TRACE(3, i);
             mbar_wait(bar_q_full(st1), ph1);
@@ -269,9 +279,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         }
         mma_commit(bar_acc);
       }
-    } else if (warp >= 4 && warp < 12) {
+    } else if (warp >= 4) {
       // -------------------------------------------------------------- compute warpgroups
-      const int wg = (warp - 4) / 4;            // query columns [64 wg, 64 wg + 64)
+      const int wg = (warp - 4) / 4;            // query columns [16 wg, +16) of each half
       const int wq = warp % 4;
       const int kr = wq * 32 + lane;            // key row within the tile
       const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
@@ -284,29 +294,29 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         mbar_wait(bar_s_full, i & 1);
         if (lane == 0 && wq == 0 && wg == 0) TRACE(5, i);
         tc_fence_after();
-#pragma unroll 1
+        const int qbase = a.j * a.c + w.qt * BQ;   // absolute position of query column 0
+#pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
-          const int c0 = 64 * hf + 32 * wg;       // this warpgroup's 32 query columns of half hf
-          uint32_t sv[32], dpv[32];
-          tmem_ld32(tmem + lane_addr + R0 + c0, sv);
-          tmem_ld32(tmem + lane_addr + R1 + c0, dpv);
-          const uint32_t nl_s = sStats + (st * 2 * BQ + c0) * 4;
+          const int c = 64 * hf + 16 * wg;        // this warp's 16 query columns of half hf
+          uint32_t sv[16], dpv[16];
+          tmem_ld16(tmem + lane_addr + R0 + c, sv);
+          tmem_ld16(tmem + lane_addr + R1 + c, dpv);
+          const uint32_t nl_s = sStats + (st * 2 * BQ + c) * 4;
           const uint32_t d_s = nl_s + BQ * 4;
-          const int qpos0 = a.j * a.c + w.qt * BQ + c0;   // absolute position of column c0
+          const int qpos0 = qbase + c;
           const bool masked = (k0 + wq * 32 + 31) > qpos0;
           tmem_wait_ld();
           if (lane == 0 && wq == 0 && wg == 0) TRACE(10 + 2 * hf, i);
-          uint32_t pp[16], dd[16];
+          uint32_t pp[8], dd[8];
           if (!masked) {
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
+            for (int c4 = 0; c4 < 4; ++c4) {
               const float4 L = ld_shared_f4(nl_s + c4 * 16), Dv = ld_shared_f4(d_s + c4 * 16);
 #pragma unroll
               for (int h2 = 0; h2 < 2; ++h2) {
                 const int c2 = c4 * 4 + h2 * 2;
                 const f2_t x = ffma2(f2u(sv[c2], sv[c2 + 1]), sl2x2, h2 ? f2(L.z, L.w) : f2(L.x, L.y));
-                const bool emu = ((c2 / 2) * kEmuPairs) / 16 != ((c2 / 2 + 1) * kEmuPairs) / 16;
-                const f2_t p2 = emu ? ex2_emu2(x) : f2(ex2(f2lo(x)), ex2(f2hi(x)));
+                const f2_t p2 = f2(ex2(f2lo(x)), ex2(f2hi(x)));
                 const f2_t ds2 = fmul2(p2, fsub2(f2u(dpv[c2], dpv[c2 + 1]), h2 ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y)));
                 pp[c2 / 2] = pack_bf16_f2(p2);
                 dd[c2 / 2] = pack_bf16_f2(ds2);
@@ -314,7 +324,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
+            for (int c4 = 0; c4 < 4; ++c4) {
               const float4 L = ld_shared_f4(nl_s + c4 * 16), Dv = ld_shared_f4(d_s + c4 * 16);
 #pragma unroll
               for (int h2 = 0; h2 < 2; ++h2) {
@@ -331,14 +341,13 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
             }
           }
           if (lane == 0 && wq == 0 && wg == 0) TRACE(11 + 2 * hf, i);
-          // P^T, dS^T (bf16) over this warpgroup's own S^T / dP^T columns just read: [c0, c0 + 16)
-          tmem_st16(tmem + lane_addr + R0 + c0, pp);
-          tmem_st16(tmem + lane_addr + R1 + c0, dd);
-          // dS^T to smem for dQ^T: box hf (query half), row kr, 16-B chunks 4 wg .. 4 wg + 3
+          // P^T, dS^T (bf16 pairs) over this warp's own S^T / dP^T columns just read: [c, c + 8)
+          tmem_st8(tmem + lane_addr + R0 + c, pp);
+          tmem_st8(tmem + lane_addr + R1 + c, dd);
+          // dS^T to smem for dQ^T: box hf (query half), row kr, 16-B chunks 2 wg, 2 wg + 1
           const uint32_t drow = sDS + hf * kBox;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            st_shared_v4(drow + sw128_off(kr, 4 * wg + q), dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]);
+          st_shared_v4(drow + sw128_off(kr, 2 * wg), dd[0], dd[1], dd[2], dd[3]);
+          st_shared_v4(drow + sw128_off(kr, 2 * wg + 1), dd[4], dd[5], dd[6], dd[7]);
           tmem_wait_st();
           fence_async_smem();
           tc_fence_before();
@@ -347,42 +356,42 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           if (lane == 0) mbar_arrive(bar_ds_half(hf));
         }
         // dQ^T(i) read-out (the compute warps are idle until S^T(i+1) lands): lane = head dim
-        // d = 32 wq + lane, this warpgroup's 64 query columns -> registers -> R0 released ->
-        // smem staging box (d / 32) = Q(i) buffer (d < 64) or dO(i) buffer (d >= 64), both dead
-        // once dQ^T(i) completed; rows = query, 128B-swizzled [128 q][32 fp32].
+        // d = 32 wq + lane, this warpgroup's 32 query columns [32 wg, +32) -> registers -> R0
+        // released -> row-major [128 q][128 d] fp32 staging over the Q(i) and dO(i) buffers
+        // (contiguous; rows 0-63 in Q's, 64-127 in dO's), both dead once dQ^T(i) completed.
         mbar_wait(bar_dq_full, i & 1);
+        if (lane == 0 && wq == 0 && wg == 0) TRACE(14, i);
         tc_fence_after();
-        uint32_t qa[32], qb[32];
-        tmem_ld32(tmem + lane_addr + R0 + 64 * wg, qa);
-        tmem_ld32(tmem + lane_addr + R0 + 64 * wg + 32, qb);
+        uint32_t qa[32];
+        tmem_ld32(tmem + lane_addr + R0 + 32 * wg, qa);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_dq_empty);
-        // row-major [128 q][128 d] fp32: rows 0-63 (warpgroup 0) land in Q(i)'s buffer, rows
-        // 64-127 (warpgroup 1) in dO(i)'s; 32 lanes store 128 contiguous bytes (conflict-free)
-        const uint32_t rowb = qbuf(st) + (uint32_t)(64 * wg) * 512 + (uint32_t)(32 * wq + lane) * 4;
+        if (lane == 0 && wq == 0 && wg == 0) TRACE(15, i);
+        // 32 lanes store 128 contiguous bytes of one row (conflict-free)
+        const uint32_t rowb = qbuf(st) + (uint32_t)(32 * wg) * 512 + (uint32_t)(32 * wq + lane) * 4;
 #pragma unroll
         for (int q = 0; q < 32; ++q) st_shared_f32(rowb + q * 512, __uint_as_float(qa[q]));
-#pragma unroll
-        for (int q = 0; q < 32; ++q) st_shared_f32(rowb + (32 + q) * 512, __uint_as_float(qb[q]));
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_stg_half(wg));
+        if (lane == 0) mbar_arrive(bar_stg_half(wg >> 1));
       }
-      // final: dK (warpgroup 0) / dV (warpgroup 1): TMEM -> scaled fp32 in smem (128B-swizzled
-      // boxes [128 keys][32 fp32]) -> TMA reduce-add into dkv.  dK stages in the Q buffers,
-      // dV in the dO buffers: free once every MMA has completed and the drain is done.
+      // final: dK (warpgroups 0, 1) / dV (warpgroups 2, 3), two 32-column chunks each: TMEM ->
+      // scaled fp32 in smem (128B-swizzled boxes [128 keys][32 fp32]) -> TMA reduce-add into
+      // dkv.  dK stages in the Q buffers, dV in the dO buffers: free once every MMA has
+      // completed and the drain is done.
       mbar_wait(bar_acc, 0);
       mbar_wait(bar_drain_done, 0);
       tc_fence_after();
-      const float sc = wg == 0 ? a.dk_scale : a.dv_scale;
-      // 4 boxes of 16 KiB: dK in the two Q buffers, dV in the two dO buffers (1024-B aligned)
-      auto stg_box = [&](int cc) { return (wg == 0 ? qbuf(cc >> 1) : dobuf(cc >> 1)) + (uint32_t)(cc & 1) * kBox; };
+      const int mat = wg >> 1;                  // 0 = dK, 1 = dV
+      const float sc = mat == 0 ? a.dk_scale : a.dv_scale;
+      auto stg_box = [&](int cc) { return (mat == 0 ? qbuf(cc >> 1) : dobuf(cc >> 1)) + (uint32_t)(cc & 1) * kBox; };
 #pragma unroll 1
-      for (int cc = 0; cc < D / 32; ++cc) {
+      for (int c2 = 0; c2 < 2; ++c2) {
+        const int cc = 2 * (wg & 1) + c2;
         uint32_t v[32];
-        tmem_ld32(tmem + lane_addr + (wg == 0 ? TM_DK : TM_DV) + cc * 32, v);
+        tmem_ld32(tmem + lane_addr + (mat == 0 ? TM_DK : TM_DV) + cc * 32, v);
         tmem_wait_ld();
         const uint32_t box = stg_box(cc);
 #pragma unroll
@@ -393,20 +402,20 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
                        __float_as_uint(sc * __uint_as_float(v[4 * q + 3])));
       }
       fence_async_smem();
-      named_bar_sync(2 + wg, 128);
-      if (wq == 0 && lane == 0) {
-        const int row0 = (wg * a.hkv + g) * a.S + k0;
+      named_bar_sync(2 + mat, 256);
+      if ((wg & 1) == 0 && wq == 0 && lane == 0) {
+        const int row0 = (mat * a.hkv + g) * a.S + k0;
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
         bulk_commit();
         bulk_wait0();
       }
-    } else if (warp >= 12) {
+    } else if (warp == 3) {
       // -------------------------------------------------------------- dQ reduce
       // once the compute warps have staged dQ^T(i) (Q(i) and dO(i) buffers), one thread
       // issues the TMA reduce-add into dQacc rows [h c + 128 qt, +128) and, when the TMA
       // has read the staging, releases both buffers to the producer.
-      if (warp == 12 && lane == 0) {
+      if (lane == 0) {
         Walk w = walk0;
         for (int i = 0; i < n; ++i, w.next()) {
           const int st = i & 1;
@@ -421,6 +430,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           bulk_reduce_add_f32(dst, qbuf(st), kTile);
           bulk_commit();
           bulk_wait_read<1>();
+          TRACE(18, i);
           mbar_arrive(bar_do_empty(st));
           bulk_wait_read<0>();
           TRACE(8, i);

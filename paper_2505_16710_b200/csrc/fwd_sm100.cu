@@ -64,7 +64,7 @@ struct Args {
   float* part_lse;            // nsplit > 1: [nsplit][hq][c] partial LSE (natural log)
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters]
 };
-constexpr int kTraceCtas = 2, kTraceSlots = 12, kTraceIters = 256;
+constexpr int kTraceCtas = 2, kTraceSlots = 24, kTraceIters = 256;
 }  // namespace fwd
 
 template <int NH, int D, int STAGES>
@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           const CUtensorMap* m = w == 0 ? &tm_k : &tm_v;
           for (int x = 0; x < HALVES; ++x)
             tma_load_3d(sKV + slot * L::kTileBytes + x * BOX, m, bar_kv_full(slot), x * 64, t * fwd::BN, g);
+          FTRACE(16 + w, t - t0);
           if (++slot == STAGES) { slot = 0; phase ^= 1; }
         }
       }
@@ -183,15 +184,18 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       for (int t = 0; t < nT; ++t) {   // t counts this CTA's tiles
         const int vslot = slot;
         mbar_wait(bar_kv_full(vslot), phase);
+        FTRACE(10, t);
         if (++slot == STAGES) { slot = 0; phase ^= 1; }
         const int kslot = slot;
         const bool more = t + 1 < nT;
         for (int b = 0; b < NH; ++b) {
+          if (b == 0) FTRACE(18, t);
           mbar_wait(bar_p_half(b, 0), t & 1);
           FTRACE(0 + b, t);
           tc_fence_after();
           issue_pv_half(b, vslot, 0, t > 0);
           mbar_wait(bar_p_half(b, 1), t & 1);
+          FTRACE(11 + 3 * b, t);
           tc_fence_after();
           issue_pv_half(b, vslot, 1, true);
           mma_commit(bar_o_full(b));
@@ -207,6 +211,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           mma_commit(bar_kv_empty(kslot));
           if (++slot == STAGES) { slot = 0; phase ^= 1; }
         }
+        FTRACE(15, t);
       }
     }
   } else if (warp >= 4) {
@@ -288,6 +293,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p_half(b, hf));
+        if (hf == 0 && lane == 0 && wq == 0) FTRACE(12 + b, t);
       };
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {

@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 lib = _lib.load()
 lib.seco_debug_trace_ptr.restype = ctypes.c_void_p
 ptr = lib.seco_debug_trace_ptr()
-CT, SL, IT = 4, 14, 128
+CT, SL, IT = 4, 20, 128
 host = np.zeros((CT, SL, IT), dtype=np.uint64)
 cudart = ctypes.CDLL("libcudart.so.12")
 cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
@@ -57,5 +57,17 @@ for cta in range(2):
         b = t[cta, 5, i]
         print(f"    compute detail i={i}: r0_ld={t[cta,10,i]-b} r0_math={t[cta,11,i]-b} r1_ld={t[cta,12,i]-b} "
               f"r1_math={t[cta,13,i]-b} arrive={t[cta,6,i]-b}")
+    print("    timeline rel. to compute s_full(i): ds0 MMAseen_ds0 ds1 MMAseen_ds1 dQcommit dPissued "
+          "dq_full_seen dq_empty_arr MMAseen_dq_empty S_issued s_full(i+1)")
+    for i in range(2, 8):
+        b = t[cta, 5, i]
+        ds0 = t[cta, 13, i] if False else 0
+        vals = [t[cta, 11, i], t[cta, 1, i], t[cta, 6, i], t[cta, 16, i], t[cta, 2, i], t[cta, 17, i],
+                t[cta, 14, i], t[cta, 15, i], t[cta, 3, i], t[cta, 4, i], t[cta, 5, i + 1]]
+        print("     i=%d " % i + " ".join("%6d" % (x - b) for x in vals))
+    print("    drain rel. to s_full(i): stg1(i-1)->reduce issued, dO half read(i-1), -, Q half read(i-1)")
+    for i in range(2, 8):
+        b = t[cta, 5, i]
+        print("     i=%d %6d %6d %6d %6d" % (i, t[cta, 7, i - 1] - b, t[cta, 18, i - 1] - b, t[cta, 19, i] - b, t[cta, 8, i - 1] - b))
     per = np.diff(t[cta, 1, :n])
     print(f"  mean period {per.mean():.0f} cycles over {n} iterations (128 query rows each); MMA ideal 2560")
