@@ -64,6 +64,11 @@ constexpr int kTmemSlot = kBar + 8 * kNumBars;
 constexpr int kBytes = kTmemSlot + 16;
 constexpr int kThreads = 640;   // 4 role warps + 4 compute warpgroups
 constexpr int kWG = 4;          // compute warpgroups; WG w owns query columns {16w + 64hf}
+// dQ drain: one thread issues TMA bulk reduce-adds.  (Tried: warps 2-3 moving the tile with
+// ld.shared + red.global.add.v4 to keep the TMA unit free for loads -- 10-15 % slower, the
+// reds clog the MIO queue that the mbarrier traffic of every role also uses.)
+constexpr int kDrainArrivals = 1;
+
 constexpr int R0 = 0, R1 = 128, TM_DK = 256, TM_DV = 384;
 #ifndef SECO_BWD_EMU
 #define SECO_BWD_EMU 0
@@ -154,9 +159,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
     mbar_init(bar_kv, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_q_full(s), 1);
-      mbar_init(bar_q_empty(s), 2);     // dK has consumed Q, and the dQ drain is done with it
+      mbar_init(bar_q_empty(s), 1 + kDrainArrivals);   // dK has consumed Q, the dQ drain has read it
       mbar_init(bar_do_full(s), 1);
-      mbar_init(bar_do_empty(s), 2);    // dV has consumed dO, and the dQ drain is done with it
+      mbar_init(bar_do_empty(s), 1 + kDrainArrivals);  // dV has consumed dO, the dQ drain has read it
     }
     mbar_init(bar_s_full, 1);
     mbar_init(bar_ds_half(0), 4 * kWG);  // one elected lane per compute warp
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
     mbar_init(bar_stg_half(0), 2 * 4);  // the 8 warps staging dQ rows [64h, 64h + 64)
     mbar_init(bar_stg_half(1), 2 * 4);
     mbar_init(bar_acc, 1);
-    mbar_init(bar_drain_done, 1);
+    mbar_init(bar_drain_done, kDrainArrivals);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           mbar_expect_tx(bar_do_full(st), kTile);
           for (int x = 0; x < D / 64; ++x)
             tma_load_3d(dobuf(st) + x * kBox, &tm_do, bar_do_full(st), x * 64, qt * BQ, h);
+          TRACE(19, i);
           mbar_wait(bar_q_empty(st), ph ^ 1);
           mbar_expect_tx(bar_q_full(st), kTile + 2 * BQ * 4);
           for (int x = 0; x < D / 64; ++x)
@@ -422,6 +428,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           const int h = g * a.G + w.hh, qt = w.qt;
           float* dst = a.dqacc + ((int64_t)h * a.c + qt * BQ) * D;   // 128 contiguous dQacc rows
           // rows 64-127 (in dO(i)'s buffer) first: dP(i+2) needs that buffer before S(i+2) needs Q's
+          // (the TMA unit serves requests in order and loads queue behind these; issuing the
+          // tile in 4-16 KiB pieces with <= 2 in flight measured 2-20 % slower)
           mbar_wait(bar_stg_half(1), i & 1);
           TRACE(7, i);
           bulk_reduce_add_f32(dst + 64 * D, dobuf(st), kTile);

@@ -68,6 +68,8 @@ for cta in range(2):
     print("    drain rel. to s_full(i): stg1(i-1)->reduce issued, dO half read(i-1), -, Q half read(i-1)")
     for i in range(2, 8):
         b = t[cta, 5, i]
-        print("     i=%d %6d %6d %6d %6d" % (i, t[cta, 7, i - 1] - b, t[cta, 18, i - 1] - b, t[cta, 19, i] - b, t[cta, 8, i - 1] - b))
+        print("     i=%d %6d %6d %6d %6d | dO(i+1) load issued %6d, Q(i+1) issued %6d, dP(i+1) issued %6d" % (
+            i, t[cta, 7, i - 1] - b, t[cta, 18, i - 1] - b, 0, t[cta, 8, i - 1] - b,
+            t[cta, 19, i + 1] - b, t[cta, 0, i + 1] - b, t[cta, 17, i] - b))
     per = np.diff(t[cta, 1, :n])
     print(f"  mean period {per.mean():.0f} cycles over {n} iterations (128 query rows each); MMA ideal 2560")
