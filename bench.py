@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--allreduce", action="store_true",
                     help="batch mode: all_reduce a LLaMA3-8B LoRA r=8 fp32 gradient bucket (27.3 MB) each step")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="SECO_FLAG_DETERMINISTIC: bit-reproducible backward (ordered dQ reduction)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no timing output")
@@ -204,7 +206,8 @@ def main():
         pinned.append(t)
     del x
     q, kc, vc, do = (t.to(dev, non_blocking=True) for t in pinned)
-    layer = ChunkedAttention(hq_r, hkv_r, d, seq, c, dtype=torch.bfloat16, device=dev)
+    layer = ChunkedAttention(hq_r, hkv_r, d, seq, c, dtype=torch.bfloat16, device=dev,
+                             deterministic=args.deterministic)
     stream = torch.cuda.current_stream()
 
     def sampled():
@@ -239,6 +242,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches = 0
+    mem_before = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
     clk = ClockSampler(local_rank)
     with clk:
         t_start.record(stream)
@@ -260,6 +265,8 @@ def main():
     if world > 1:
         dist.barrier()
     ms_local = t_start.elapsed_time(t_end)
+    memory = dict(layer.memory_ledger())
+    memory["allocated_during_timed_steps_bytes"] = torch.cuda.max_memory_allocated(dev) - mem_before
     t_f = t_b = 0.0
     for s in range(args.steps):
         for n, (kind, j) in enumerate(order):
@@ -316,7 +323,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         sets = [(q, kc, vc, do), tuple(torch.empty_like(t) for t in (q, kc, vc, do))]
-        layers = [layer, ChunkedAttention(hq_r, hkv_r, d, seq, c, dtype=torch.bfloat16, device=dev)]
+        layers = [layer, ChunkedAttention(hq_r, hkv_r, d, seq, c, dtype=torch.bfloat16, device=dev,
+                                          deterministic=args.deterministic)]
         out_dq = [torch.empty(layer.dq.shape, dtype=layer.dq.dtype).pin_memory() for _ in range(2)]
         out_dkv = [torch.empty(layer.dkv.shape, dtype=layer.dkv.dtype).pin_memory() for _ in range(2)]
         h2d = sum(t.numel() * t.element_size() for t in pinned)
@@ -380,13 +388,13 @@ def main():
                                    f"{args.mode}" + (f" t={args.t} of {k} (I={sel}, gamma={gamma})"
                                                      if sel is not None else ""),
                        "hq": hq, "hkv": hkv, "d": d, "seq_len": seq, "chunk": c, "num_chunks": k,
-                       "mode": args.mode, "sequences_per_step": n_seq,
+                       "mode": args.mode, "sequences_per_step": n_seq, "deterministic": args.deterministic,
                        "parallelism": f"{args.shard}{world}" if world > 1 else "single",
                        "allreduce_bytes_per_step": (LORA_PARAMS_LLAMA3_8B_R8 * 4 if args.allreduce else 0),
                        "l2_policy": "inputs larger than L2 (Q,dO 256 MiB, K,V 64 MiB each, dKV 256 MiB per rank)"},
             "tokens_per_s": tokens / (ms_per_step * 1e-3),
             "step_tflop": total_flops / 1e12,
-            "roofline": roofline, "kernels": kern,
+            "roofline": roofline, "kernels": kern, "memory": memory,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -71,7 +71,17 @@ typedef struct {
   seco_dtype dtype;
   int64_t q_head_stride, q_row_stride;   /* for q, o, d_o, dq                     */
   int64_t kv_head_stride, kv_row_stride; /* for k_cache, v_cache                  */
+  int32_t flags;            /* SECO_FLAG_* (0 = default)                          */
 } seco_shape;
+
+/* flags: SECO_FLAG_DETERMINISTIC makes every call bit-reproducible for identical
+ * inputs (the paper attributes its SeCO-vs-baseline mismatch to
+ * atomic accumulation).  The backward then adds the per-key-tile dQ
+ * partials of each query tile in ascending key-tile order (per-tile counters in
+ * the workspace, one owner per dK/dV tile, no Q-split); the forward is
+ * deterministic in every mode (one writer per output, fixed-order split-KV
+ * combine).  Costs backward throughput: the first wave of CTAs orders itself. */
+#define SECO_FLAG_DETERMINISTIC 1
 
 /* Bytes of device workspace `ws` the two chunk calls need (dQ accumulator,
  * row statistics).  Same for every j. */

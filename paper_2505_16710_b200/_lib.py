@@ -22,7 +22,11 @@ class SecoShape(ctypes.Structure):
                 ("chunk", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("softmax_scale", ctypes.c_float), ("dtype", ctypes.c_int32),
                 ("q_head_stride", ctypes.c_int64), ("q_row_stride", ctypes.c_int64),
-                ("kv_head_stride", ctypes.c_int64), ("kv_row_stride", ctypes.c_int64)]
+                ("kv_head_stride", ctypes.c_int64), ("kv_row_stride", ctypes.c_int64),
+                ("flags", ctypes.c_int32)]
+
+
+SECO_FLAG_DETERMINISTIC = 1
 
 
 class SecoError(RuntimeError):

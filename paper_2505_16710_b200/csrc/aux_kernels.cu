@@ -32,6 +32,8 @@ struct PrepArgs {
   int64_t qh, qr;
   float relay;
   int nD, nR, nZ;  // block counts of the three tasks
+  int* order;      // deterministic mode: dQ order counters [hq][c/128] to zero (else null)
+  int n_order;
 };
 
 // Task A (blocks [0,nD)): one warp per (h, row): D = sum_x dO*O (and -LSE log2 e for the
@@ -72,6 +74,8 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
     }
   } else {
     if (dqacc == nullptr) return;
+    if (a.order && bid == a.nD + a.nR)
+      for (int i = threadIdx.x; i < a.n_order; i += blockDim.x) a.order[i] = 0;
     const int64_t total = (int64_t)a.hq * a.c * a.d / 4;
     float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t i = (int64_t)(bid - a.nD - a.nR) * blockDim.x + threadIdx.x; i < total;
@@ -137,13 +141,15 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
 
 template <typename T>
 static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, float* D, float* dkv, float* dqacc,
-                               const float* lse, float* nlse, float relay, cudaStream_t st) {
+                               const float* lse, float* nlse, float relay, cudaStream_t st, int* order = nullptr) {
   PrepArgs a;
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
   a.qh = g.qh; a.qr = g.qr; a.relay = relay;
   a.nD = (g.hq * g.c + 7) / 8;
   a.nR = relay == 1.f ? 0 : 296;
   a.nZ = dqacc ? 296 : 0;
+  a.order = order;
+  a.n_order = g.hq * ((g.c + 127) / 128);
   bwd_prep_kernel<T><<<a.nD + a.nR + a.nZ, 256, 0, st>>>(o, d_o, D, dkv, dqacc, lse, nlse, a);
   return cudaGetLastError();
 }
@@ -163,10 +169,11 @@ static cudaError_t launch_final(const ChunkGeom& g, const float* dqacc, T* dq, c
 
 // bf16 path helpers, used by launch_bwd_sm100
 cudaError_t launch_prep_bf16(const ChunkGeom& g, const void* o, const void* d_o, float* D, float* dkv,
-                             float* dqacc, const float* lse, float* nlse, float relay, cudaStream_t st) {
+                             float* dqacc, const float* lse, float* nlse, float relay, cudaStream_t st,
+                             int* order) {
   return launch_prep<__nv_bfloat16>(g, reinterpret_cast<const __nv_bfloat16*>(o),
                                     reinterpret_cast<const __nv_bfloat16*>(d_o), D, dkv, dqacc, lse, nlse, relay,
-                                    st);
+                                    st, order);
 }
 cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, const float* dkv, void* dk_own,
                               void* dv_own, float dq_scale, cudaStream_t st) {

@@ -41,7 +41,8 @@ extern "C" void* seco_debug_trace_ptr() { return seco_trace_buffer; }
 #endif
 
 cudaError_t launch_prep_bf16(const ChunkGeom& g, const void* o, const void* d_o, float* D, float* dkv,
-                             float* dqacc, const float* lse, float* nlse, float relay, cudaStream_t st);
+                             float* dqacc, const float* lse, float* nlse, float relay, cudaStream_t st,
+                             int* order);
 cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, const float* dkv, void* dk_own,
                               void* dv_own, float dq_scale, cudaStream_t st);
 
@@ -85,6 +86,8 @@ struct Args {
   const float* nlse;  // [hq][c]  -LSE * log2(e)   (from bwd_prep)
   const float* Dv;    // [hq][c]  rowsum(dO o O)  (from bwd_prep)
   float* dqacc;       // [hq][c][D] fp32 dQ accumulator (zeroed by bwd_prep)
+  int* dq_order;      // deterministic mode: [hq][c/BQ] count of key tiles that have added their
+                      // dQ share of query tile (h, qt) (zeroed by bwd_prep); null otherwise
   int* err;           // set to 1 if the dynamic smem window is not 1024-B aligned
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters] clock64
 };
@@ -430,11 +433,23 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           // rows 64-127 (in dO(i)'s buffer) first: dP(i+2) needs that buffer before S(i+2) needs Q's
           // (the TMA unit serves requests in order and loads queue behind these; issuing the
           // tile in 4-16 KiB pieces with <= 2 in flight measured 2-20 % slower)
+          int* ctr = a.dq_order ? a.dq_order + (int64_t)h * nqt + qt : nullptr;
           mbar_wait(bar_stg_half(1), i & 1);
           TRACE(7, i);
+          if (ctr) {
+            // deterministic mode: the key tiles seeing query tile qt are 0 .. j c / BKV + qt;
+            // add after tiles 0 .. u-1 have (fixed fp32 summation order).  Both staging
+            // phases are consumed before the (possibly long) wait, so the compute warps can
+            // never run a full phase ahead of this thread on the stg barriers.
+            mbar_wait(bar_stg_half(0), i & 1);
+            while (ld_relaxed_gpu(ctr) != u) {
+            }
+            fence_acq_rel_gpu();
+            fence_proxy_async_global();      // ... before this thread's TMA reduce-adds
+          }
           bulk_reduce_add_f32(dst + 64 * D, dobuf(st), kTile);
           bulk_commit();
-          mbar_wait(bar_stg_half(0), i & 1);
+          if (!ctr) mbar_wait(bar_stg_half(0), i & 1);
           bulk_reduce_add_f32(dst, qbuf(st), kTile);
           bulk_commit();
           bulk_wait_read<1>();
@@ -443,6 +458,11 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           bulk_wait_read<0>();
           TRACE(8, i);
           mbar_arrive(bar_q_empty(st));
+          if (ctr) {
+            bulk_wait0();                    // the reduce-adds have been performed in L2
+            fence_proxy_async_global();
+            st_release_gpu(ctr, u + 1);
+          }
         }
         bulk_wait0();
         mbar_arrive(bar_drain_done);
@@ -463,7 +483,8 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st, int* launches) {
   static_assert(bwd::kBytes <= 232448, "shared memory budget");
   if (g.d != bwd::D || g.c % bwd::BQ) return cudaErrorInvalidValue;
-  cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.c, relay, st);
+  int* order = g.det ? reinterpret_cast<int*>(ws_D + 2 * (size_t)g.hq * g.c) : nullptr;
+  cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.c, relay, st, order);
   if (e != cudaSuccess) return e;
   static bool attr_set = false;
   if (!attr_set) {
@@ -476,7 +497,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.dk_scale = gscale * g.scale;
   a.dv_scale = gscale;
-  a.nlse = ws_D + (size_t)g.hq * g.c; a.Dv = ws_D; a.dqacc = ws_dqacc;
+  a.nlse = ws_D + (size_t)g.hq * g.c; a.Dv = ws_D; a.dqacc = ws_dqacc; a.dq_order = order;
   a.err = nullptr;
   a.trace = nullptr;
 #ifdef SECO_TRACE
@@ -494,7 +515,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   // at least one query tile (the shortest, diagonal key tile has G of them).
   int nsplit = (2 * 148 + ntiles * g.hkv - 1) / (ntiles * g.hkv);
   if (nsplit > a.G) nsplit = a.G;
-  if (nsplit < 1) nsplit = 1;
+  if (nsplit < 1 || g.det) nsplit = 1;   // deterministic: one owner per dK/dV tile
   a.nsplit = nsplit;
   dim3 grid(ntiles * nsplit * g.hkv);
   seco_bwd_sm100_kernel<<<grid, bwd::kThreads, bwd::kBytes, st>>>(tq, tdo, tk, tv, tdq, tdkv, a);

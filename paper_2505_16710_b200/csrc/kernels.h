@@ -12,6 +12,7 @@ struct ChunkGeom {
   float scale;               // softmax scale sigma
   int64_t qh, qr;            // q/o/do/dq strides (elements)
   int64_t kh, kr;            // k/v cache strides (elements)
+  bool det = false;          // SECO_FLAG_DETERMINISTIC: ordered dQ reduction, no Q-split
 };
 
 // ---- fp32 debug path (SIMT FFMA, any d <= 256, any c) -------------------------------

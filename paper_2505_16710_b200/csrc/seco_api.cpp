@@ -110,6 +110,7 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
   } else {
     return fail(SECO_ERR_ARG, "unknown dtype %d", (int)s->dtype);
   }
+  if (s->flags & ~SECO_FLAG_DETERMINISTIC) return fail(SECO_ERR_ARG, "unknown flags 0x%x", (unsigned)s->flags);
   return SECO_OK;
 }
 
@@ -118,13 +119,16 @@ seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
   g.hq = s->hq; g.hkv = s->hkv; g.d = s->d; g.c = s->chunk; g.k = s->num_chunks; g.j = j;
   g.scale = s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt((float)s->d);
   g.qh = s->q_head_stride; g.qr = s->q_row_stride; g.kh = s->kv_head_stride; g.kr = s->kv_row_stride;
+  g.det = (s->flags & SECO_FLAG_DETERMINISTIC) != 0;
   return g;
 }
 
 size_t ws_floats(const seco_shape* s) {
   // backward: dQ accumulator [hq][c][d] + D [hq][c] + (-LSE log2 e) [hq][c]
+  //           + (deterministic mode) dQ order counters [hq][ceil(c/128)] int32
   // forward (split-KV, up to 4 parts): partial O [4][hq][c][d] + partial LSE [4][hq][c]
-  const size_t bwd = (size_t)s->hq * s->chunk * s->d + 2 * (size_t)s->hq * s->chunk;
+  const size_t bwd = (size_t)s->hq * s->chunk * s->d + 2 * (size_t)s->hq * s->chunk +
+                     (size_t)s->hq * ((s->chunk + 127) / 128);
   const size_t fwd = 4 * (size_t)s->hq * s->chunk * (s->d + 1);
   return bwd > fwd ? bwd : fwd;
 }

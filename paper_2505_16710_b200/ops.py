@@ -13,8 +13,10 @@ from ._lib import SecoShape, check, load
 _DTYPES = {torch.bfloat16: _lib.SECO_BF16, torch.float32: _lib.SECO_FP32_DEBUG}
 
 
-def make_shape(q_full: torch.Tensor, k_cache: torch.Tensor, chunk: int, softmax_scale: float = 0.0) -> SecoShape:
-    """Shape record for Q [hq][S][d] (full sequence) and a KV cache [hkv][S][d]."""
+def make_shape(q_full: torch.Tensor, k_cache: torch.Tensor, chunk: int, softmax_scale: float = 0.0,
+               deterministic: bool = False) -> SecoShape:
+    """Shape record for Q [hq][S][d] (full sequence) and a KV cache [hkv][S][d].
+    deterministic: bit-reproducible backward (SECO_FLAG_DETERMINISTIC)."""
     if q_full.dtype not in _DTYPES or k_cache.dtype != q_full.dtype:
         raise TypeError("q / k_cache must both be bf16 (tensor-core path) or float32 (debug path)")
     hq, S, d = q_full.shape
@@ -24,7 +26,8 @@ def make_shape(q_full: torch.Tensor, k_cache: torch.Tensor, chunk: int, softmax_
     if S % chunk:
         raise ValueError("sequence length must be a multiple of the chunk size")
     return SecoShape(hq, hkv, d, chunk, S // chunk, float(softmax_scale), _DTYPES[q_full.dtype],
-                     q_full.stride(0), q_full.stride(1), k_cache.stride(0), k_cache.stride(1))
+                     q_full.stride(0), q_full.stride(1), k_cache.stride(0), k_cache.stride(1),
+                     _lib.SECO_FLAG_DETERMINISTIC if deterministic else 0)
 
 
 def _stream(stream):

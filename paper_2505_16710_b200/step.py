@@ -28,7 +28,7 @@ class ChunkedAttention:
     chunk's own K / V (slot j = total own-chunk gradient after chunk j's relay)."""
 
     def __init__(self, hq, hkv, d, seq, chunk, dtype=torch.bfloat16, device="cuda", softmax_scale=0.0,
-                 own_copies=False):
+                 own_copies=False, deterministic=False):
         if seq % chunk:
             raise ValueError("seq must be a multiple of chunk")
         self.hq, self.hkv, self.d, self.seq, self.chunk = hq, hkv, d, seq, chunk
@@ -45,7 +45,7 @@ class ChunkedAttention:
         self.own = torch.empty(2, hkv, chunk, d, dtype=dtype, device=dev) if own_copies else None
         probe_q = torch.empty(hq, seq, d, dtype=dtype, device="meta")
         probe_k = torch.empty(hkv, seq, d, dtype=dtype, device="meta")
-        self.shape = ops.make_shape(probe_q, probe_k, chunk, softmax_scale)
+        self.shape = ops.make_shape(probe_q, probe_k, chunk, softmax_scale, deterministic)
         self.ws = torch.empty(max(ops.seco_workspace_size(self.shape) // 4, 1), dtype=torch.float32, device=dev)
 
     # ---- per-chunk calls -------------------------------------------------------------
@@ -109,6 +109,24 @@ class ChunkedAttention:
         r = self.step(q, k_cache, v_cache, do, idx, gamma, s, stream)
         r.selected, r.relay_scale, r.seed_scale = idx, gamma, s
         return r
+
+    def memory_ledger(self):
+        """Device bytes by role (the memory claim P:175-177, 'reduces the
+        memory requirements for storing forward activations by a factor of k').  What scales
+        with the sequence: the KV checkpoints (caller's), their fp32 gradient buffer dKV and
+        the per-token inputs / outputs.  What a chunk call needs on top: the workspace and
+        the chunk-j views of Q, O, dO, dQ, LSE -- O(c), independent of k (the library never
+        allocates; tests/test_gpu_fullsize.py checks that a step allocates nothing)."""
+        el = torch.finfo(self.dtype).bits // 8
+        hq, hkv, S, c, d = self.hq, self.hkv, self.seq, self.chunk, self.d
+        return {
+            "kv_cache_bytes": 2 * hkv * S * d * el,                     # caller-owned checkpoints
+            "dkv_fp32_bytes": self.dkv.numel() * 4,                       # persistent m'.grad
+            "q_do_bytes": 2 * hq * S * d * el,                            # caller-owned inputs
+            "o_dq_lse_bytes": (self.o.numel() + self.dq.numel()) * el + self.lse.numel() * 4,
+            "per_call_chunk_bytes": 4 * hq * c * d * el + hq * c * 4,     # Q_j, O_j, dO_j, dQ_j, LSE_j (views)
+            "per_call_workspace_bytes": self.ws.numel() * 4,
+        }
 
     @property
     def dk(self):

@@ -82,7 +82,7 @@ def test_sampler_errors(lib):
 
 def _shape(**kw):
     d = dict(hq=32, hkv=8, d=128, chunk=256, num_chunks=4, softmax_scale=0.0, dtype=0,
-             q_head_stride=1024 * 128, q_row_stride=128, kv_head_stride=1024 * 128, kv_row_stride=128)
+             q_head_stride=1024 * 128, q_row_stride=128, kv_head_stride=1024 * 128, kv_row_stride=128, flags=0)
     d.update(kw)
     return _lib.SecoShape(*[d[f] for f, _ in _lib.SecoShape._fields_])
 
@@ -100,6 +100,7 @@ def _shape(**kw):
     (dict(q_head_stride=128 * 128), 0, _lib.SECO_ERR_ARG),                  # heads overlap rows
     (dict(q_head_stride=128, q_row_stride=16 * 128), 0, _lib.SECO_ERR_ARG),  # interleaved, too few heads/row
     (dict(kv_head_stride=256 * 128), 0, _lib.SECO_ERR_ARG),                 # cache heads overlap
+    (dict(flags=2), 0, _lib.SECO_ERR_ARG),                                   # unknown flag bit
 ])
 def test_argument_validation(lib, kw, j, code):
     s = _shape(**kw)

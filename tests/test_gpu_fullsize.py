@@ -89,3 +89,29 @@ def test_cfg3_spaco_sampled_rows(cfg3):
             assert err(dq_g[h, p], r.seed_scale * ref) <= BF16_TOL
         else:
             assert np.abs(dq_g[h, p]).max() == 0.0
+
+
+def test_memory_ledger_step_allocates_nothing():
+    """a SeCO / SpaCO step allocates no device memory beyond the
+    buffers set up once, and the per-call working set (workspace + chunk views) does not grow
+    with the number of chunks k; only the O(S) checkpoint-sized buffers do."""
+    from paper_2505_16710_b200.step import ChunkedAttention
+    hq, hkv, d, c = 8, 2, 128, 256
+    ledgers = {}
+    for k in (2, 4, 8):
+        x = make_inputs(hq, hkv, k * c, d, seed=k)
+        q, kc, vc, do = upload(x, torch.bfloat16)
+        layer = ChunkedAttention(hq, hkv, d, k * c, c, dtype=torch.bfloat16)
+        layer.seco_step(q, kc, vc, do)           # warm (tensor maps, attributes)
+        torch.cuda.synchronize()
+        before = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        layer.seco_step(q, kc, vc, do)
+        layer.spaco_step(q, kc, vc, do, t=1, seed=3)
+        torch.cuda.synchronize()
+        assert torch.cuda.max_memory_allocated() == before
+        ledgers[k] = layer.memory_ledger()
+    per_call = {k: (v["per_call_chunk_bytes"], v["per_call_workspace_bytes"]) for k, v in ledgers.items()}
+    assert len(set(per_call.values())) == 1
+    assert ledgers[8]["dkv_fp32_bytes"] == 4 * ledgers[2]["dkv_fp32_bytes"]
+    assert ledgers[8]["kv_cache_bytes"] == 4 * ledgers[2]["kv_cache_bytes"]

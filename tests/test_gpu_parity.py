@@ -191,3 +191,34 @@ def test_bf16_strided_sequence_major_layout():
     assert err(host(dq), ref["dq"]) <= BF16_TOL
     assert err(host(dkv[0]), ref["dk"]) <= BF16_TOL
     assert err(host(dkv[1]), ref["dv"]) <= BF16_TOL
+
+
+@pytest.mark.parametrize("hq,hkv,seq,c", [(8, 2, 2048, 512), (4, 1, 1024, 128)])
+def test_bf16_deterministic_mode_bit_reproducible(hq, hkv, seq, c):
+    """SECO_FLAG_DETERMINISTIC: two SeCO steps and two SpaCO
+    steps on the same inputs give bit-identical O, dQ and dKV, and stay within the bf16
+    tolerance of the oracle.  These shapes use Q-split and many key tiles per query tile in
+    the default mode, so both ordering mechanisms are exercised."""
+    from paper_2505_16710_b200.step import ChunkedAttention
+    x = inputs(hq, hkv, seq, 128, seed=11)
+    q, k, v, do = upload(x, torch.bfloat16)
+    layer = ChunkedAttention(hq, hkv, 128, seq, c, dtype=torch.bfloat16, deterministic=True)
+    outs = []
+    for _ in range(2):
+        layer.seco_step(q, k, v, do)
+        torch.cuda.synchronize()
+        outs.append((layer.o.clone(), layer.dq.clone(), layer.dkv.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a.view(torch.int32),
+                           b.view(torch.int16) if b.dtype == torch.bfloat16 else b.view(torch.int32))
+    ref = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (seq // c))
+    assert err(host(layer.dq), ref["dq"]) <= BF16_TOL
+    assert err(host(layer.dkv[0]), ref["dk"]) <= BF16_TOL
+    assert err(host(layer.dkv[1]), ref["dv"]) <= BF16_TOL
+    sp = []
+    for _ in range(2):
+        layer.spaco_step(q, k, v, do, t=max(1, seq // c // 2), seed=5)
+        torch.cuda.synchronize()
+        sp.append((layer.dq.clone(), layer.dkv.clone()))
+    assert torch.equal(sp[0][0].view(torch.int16), sp[1][0].view(torch.int16))
+    assert torch.equal(sp[0][1].view(torch.int32), sp[1][1].view(torch.int32))
