@@ -43,7 +43,8 @@
  * validated on the host before any launch (SECO_ERR_ARG: null pointer, j out of
  * range, hq % hkv != 0, non-positive sizes, misaligned pointer or stride;
  * SECO_ERR_UNSUPPORTED: a shape the bf16 tensor-core path does not implement --
- * it needs d = 128, c % 128 == 0, 16-byte aligned rows; the fp32 debug
+ * it needs d in {64, 128} (64 runs on zero-padded 128-wide tiles), c % 128
+ * == 0, 16-byte aligned rows; the fp32 debug
  * path accepts any d <= 256 and any c).  Launch failures return SECO_ERR_CUDA;
  * faults during execution surface at the caller's next synchronisation.
  */

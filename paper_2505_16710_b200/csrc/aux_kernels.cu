@@ -32,6 +32,7 @@ struct PrepArgs {
   int64_t qh, qr;
   float relay;
   int nD, nR, nZ;  // block counts of the three tasks
+  int ldq;         // dQacc row stride (floats)
   int* order;      // deterministic mode: dQ order counters [hq][c/128] to zero (else null)
   int n_order;
 };
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
     if (dqacc == nullptr) return;
     if (a.order && bid == a.nD + a.nR)
       for (int i = threadIdx.x; i < a.n_order; i += blockDim.x) a.order[i] = 0;
-    const int64_t total = (int64_t)a.hq * a.c * a.d / 4;
+    const int64_t total = (int64_t)a.hq * a.c * a.ldq / 4;
     float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t i = (int64_t)(bid - a.nD - a.nR) * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)a.nZ * blockDim.x)
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
 
 struct FinalArgs {
   int hq, hkv, c, d, j, S;
+  int ldq;         // dQacc row stride (floats)
   int64_t qh, qr;
   float dq_scale;  // s * sigma
   int nQ, nO;
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
                                                         const float* __restrict__ dkv, T* __restrict__ dk_own,
                                                         T* __restrict__ dv_own, FinalArgs a) {
   const int bid = blockIdx.x;
-  const int dv4 = a.d / 4;
+  const int dv4 = a.d / 4, ld4 = a.ldq / 4;
   if (bid < a.nQ) {
     if (dqacc == nullptr) return;
     const int64_t rows = (int64_t)a.hq * a.c;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
       const int64_t row = i / dv4;
       const int x = (int)(i - row * dv4) * 4;
       const int64_t h = row / a.c, r = row - h * a.c;
-      float4 v = reinterpret_cast<const float4*>(dqacc)[i];
+      float4 v = reinterpret_cast<const float4*>(dqacc)[row * ld4 + x / 4];
       v.x *= a.dq_scale; v.y *= a.dq_scale; v.z *= a.dq_scale; v.w *= a.dq_scale;
       Vec4<T>::store(dq + h * a.qh + r * a.qr + x, v);
     }
@@ -149,6 +151,7 @@ static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, flo
   a.nR = relay == 1.f ? 0 : 296;
   a.nZ = dqacc ? 296 : 0;
   a.order = order;
+  a.ldq = g.ldq ? g.ldq : g.d;
   a.n_order = g.hq * ((g.c + 127) / 128);
   bwd_prep_kernel<T><<<a.nD + a.nR + a.nZ, 256, 0, st>>>(o, d_o, D, dkv, dqacc, lse, nlse, a);
   return cudaGetLastError();
@@ -159,7 +162,7 @@ static cudaError_t launch_final(const ChunkGeom& g, const float* dqacc, T* dq, c
                                 T* dv_own, float dq_scale, cudaStream_t st) {
   FinalArgs a;
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
-  a.qh = g.qh; a.qr = g.qr; a.dq_scale = dq_scale;
+  a.qh = g.qh; a.qr = g.qr; a.dq_scale = dq_scale; a.ldq = g.ldq ? g.ldq : g.d;
   a.nQ = dqacc ? 296 : 0;
   a.nO = (dk_own || dv_own) ? 148 : 0;
   if (a.nQ + a.nO == 0) return cudaSuccess;
@@ -186,7 +189,7 @@ cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, 
 // O = sum_s exp(LSE_s - LSE) O_s,  LSE = log sum_s exp(LSE_s)   (exact merge of softmax partials
 // over disjoint key ranges).  One warp per (head, row); each lane owns 4 of the d = 128 columns.
 struct CombArgs {
-  int hq, c, nsplit;
+  int hq, c, nsplit, d;
   int64_t qh, qr;
 };
 __global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restrict__ part_o,
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restric
     acc.x += wt * v.x; acc.y += wt * v.y; acc.z += wt * v.z; acc.w += wt * v.w;
   }
   const float inv = 1.f / den;
+  if (4 * lane >= a.d) { if (lane == 0) lse[w] = mx + __logf(den); return; }
   uint2 pk;
   pk.x = pack_bf16(acc.x * inv, acc.y * inv);
   pk.y = pack_bf16(acc.z * inv, acc.w * inv);
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restric
 cudaError_t launch_fwd_combine(const ChunkGeom& g, int nsplit, const float* part_o, const float* part_lse, void* o,
                                float* lse, cudaStream_t st) {
   CombArgs a;
-  a.hq = g.hq; a.c = g.c; a.nsplit = nsplit; a.qh = g.qh; a.qr = g.qr;
+  a.hq = g.hq; a.c = g.c; a.nsplit = nsplit; a.qh = g.qh; a.qr = g.qr; a.d = g.d;
   fwd_combine_kernel<<<(g.hq * g.c + 7) / 8, 256, 0, st>>>(part_o, part_lse, reinterpret_cast<__nv_bfloat16*>(o),
                                                             lse, a);
   return cudaGetLastError();

@@ -482,7 +482,9 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              const float* lse, float relay, float gscale, float* dkv, void* dq, void* dk_own,
                              void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st, int* launches) {
   static_assert(bwd::kBytes <= 232448, "shared memory budget");
-  if (g.d != bwd::D || g.c % bwd::BQ) return cudaErrorInvalidValue;
+  // d = 64 runs on zero-padded 128-column tiles (TMA out-of-bounds fill on load; the dK/dV
+  // reduce-add boxes past column 64 are dropped by the same bounds check; dQacc rows are 128)
+  if ((g.d != bwd::D && g.d != 64) || g.c % bwd::BQ) return cudaErrorInvalidValue;
   int* order = g.det ? reinterpret_cast<int*>(ws_D + 2 * (size_t)g.hq * g.c) : nullptr;
   cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.c, relay, st, order);
   if (e != cudaSuccess) return e;

@@ -58,6 +58,7 @@ struct Layout {
 struct Args {
   int c, j, hq, G, nqt, nhp;  // chunk size, chunk index, q heads, group size, q tiles, head packs
   int nsplit;                 // split-KV factor (1: final O/LSE written directly)
+  int d_out;                  // head dim of the O buffer (64: the D = 128 tile is zero-padded)
   float scale_log2;           // sigma * log2(e)
   int64_t qh, qr;             // o strides (elements)
   float* part_o;              // nsplit > 1: [nsplit][hq][c][D] fp32 normalised partial O
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)(qt * fwd::BM + r) * a.qr;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
+        if (cc * 32 >= a.d_out) break;       // warp-uniform
         uint32_t v[32];
         tmem_ld32(tO + cc * 32, v);
         tmem_wait_ld();
@@ -373,7 +375,7 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   a.c = g.c; a.j = g.j; a.hq = g.hq; a.G = g.hq / g.hkv;
   a.nqt = g.c / fwd::BM; a.nhp = g.hq / NH;
   a.scale_log2 = g.scale * 1.4426950408889634f;
-  a.qh = g.qh; a.qr = g.qr;
+  a.qh = g.qh; a.qr = g.qr; a.d_out = g.d;
   // split-KV (§8 row a9) when the chunk has too few equal-cost units (q tiles x head packs)
   // to fill the SMs -- e.g. head-sharded ranks.  Cost model in K/V-tile units per wave:
   // ~8 tiles of prologue/epilogue per work item, 15% of a unit for the fp32 partial
@@ -420,7 +422,9 @@ cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
                              cudaStream_t st, int* launches) {
   const int G = g.hq / g.hkv;
-  if (g.d == 128) {
+  // d = 64 runs the D = 128 kernel on zero-padded tiles: the tensor maps describe 64-column
+  // rows, so the TMA fills the second 64-column box of every tile with zeros
+  if (g.d == 128 || g.d == 64) {
     if (G % 2 == 0) return launch_fwd_impl<2, 128, 5>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
     return launch_fwd_impl<1, 128, 6>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
   }

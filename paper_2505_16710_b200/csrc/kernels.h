@@ -13,6 +13,8 @@ struct ChunkGeom {
   int64_t qh, qr;            // q/o/do/dq strides (elements)
   int64_t kh, kr;            // k/v cache strides (elements)
   bool det = false;          // SECO_FLAG_DETERMINISTIC: ordered dQ reduction, no Q-split
+  int ldq = 0;               // row stride (floats) of the dQ accumulator: 128 on the bf16 path
+                             // (d = 64 runs zero-padded to 128), d on the fp32 path
 };
 
 // ---- fp32 debug path (SIMT FFMA, any d <= 256, any c) -------------------------------

@@ -66,11 +66,13 @@ bool encode_3d(CUtensorMap* m, const void* ptr, int d, int rows, int heads, int6
 
 // 2-D fp32 tensor map over a dense [rows][128] matrix, box {32, box_rows}, 128-B swizzle
 // (the TMA reduce-add targets: dQ accumulator and dKV)
-bool encode_f32_rows(CUtensorMap* m, const void* ptr, int64_t rows, int box_rows) {
+// fp32 rows of `cols` floats (boxes of 32 columns; a box past `cols` is skipped by the
+// TMA's bounds check, which is how a zero-padded d = 64 tile reduces into a d = 64 buffer)
+bool encode_f32_rows(CUtensorMap* m, const void* ptr, int64_t rows, int box_rows, int cols = 128) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {128, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {128 * 4};
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
   cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
@@ -100,7 +102,8 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
       !disjoint(s->d, (int64_t)s->chunk * s->num_chunks, s->hkv, s->kv_row_stride, s->kv_head_stride))
     return fail(SECO_ERR_ARG, "strides overlap rows/heads (need head-major or row-major-interleaved rows)");
   if (s->dtype == SECO_BF16) {
-    if (s->d != 128) return fail(SECO_ERR_UNSUPPORTED, "bf16 path implements d=128 (got %d)", s->d);
+    if (s->d != 128 && s->d != 64)
+      return fail(SECO_ERR_UNSUPPORTED, "bf16 path implements d in {64, 128} (got %d)", s->d);
     if (s->chunk % 128) return fail(SECO_ERR_UNSUPPORTED, "bf16 path needs chunk %% 128 == 0 (got %d)", s->chunk);
     if ((s->q_row_stride * 2) % 16 || (s->q_head_stride * 2) % 16 || (s->kv_row_stride * 2) % 16 ||
         (s->kv_head_stride * 2) % 16)
@@ -114,12 +117,17 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
   return SECO_OK;
 }
 
+// the bf16 kernels work on 128-wide head dims (d = 64 is zero-padded by the TMA's
+// out-of-bounds fill), so their fp32 dQ accumulator rows are 128 floats
+int dq_ld(const seco_shape* s) { return s->dtype == SECO_BF16 ? 128 : s->d; }
+
 seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
   seco::ChunkGeom g;
   g.hq = s->hq; g.hkv = s->hkv; g.d = s->d; g.c = s->chunk; g.k = s->num_chunks; g.j = j;
   g.scale = s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt((float)s->d);
   g.qh = s->q_head_stride; g.qr = s->q_row_stride; g.kh = s->kv_head_stride; g.kr = s->kv_row_stride;
   g.det = (s->flags & SECO_FLAG_DETERMINISTIC) != 0;
+  g.ldq = dq_ld(s);
   return g;
 }
 
@@ -127,9 +135,9 @@ size_t ws_floats(const seco_shape* s) {
   // backward: dQ accumulator [hq][c][d] + D [hq][c] + (-LSE log2 e) [hq][c]
   //           + (deterministic mode) dQ order counters [hq][ceil(c/128)] int32
   // forward (split-KV, up to 4 parts): partial O [4][hq][c][d] + partial LSE [4][hq][c]
-  const size_t bwd = (size_t)s->hq * s->chunk * s->d + 2 * (size_t)s->hq * s->chunk +
+  const size_t bwd = (size_t)s->hq * s->chunk * dq_ld(s) + 2 * (size_t)s->hq * s->chunk +
                      (size_t)s->hq * ((s->chunk + 127) / 128);
-  const size_t fwd = 4 * (size_t)s->hq * s->chunk * (s->d + 1);
+  const size_t fwd = 4 * (size_t)s->hq * s->chunk * (dq_ld(s) + 1);
   return bwd > fwd ? bwd : fwd;
 }
 
@@ -214,7 +222,7 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   float* wsf = reinterpret_cast<float*>(ws);
   float* ws_dqacc = wsf;
-  float* ws_D = wsf + (size_t)s->hq * s->chunk * s->d;
+  float* ws_D = wsf + (size_t)s->hq * s->chunk * dq_ld(s);
   int launches = 0;
   cudaError_t e;
   if (s->dtype == SECO_FP32_DEBUG) {
@@ -235,7 +243,7 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
       !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
       !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
       !encode_f32_rows(&tdq, ws_dqacc, (int64_t)s->hq * s->chunk, 128) ||
-      !encode_f32_rows(&tdkv, dkv, 2 * (int64_t)s->hkv * S, 128))
+      !encode_f32_rows(&tdkv, dkv, 2 * (int64_t)s->hkv * S, 128, s->d))
     return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   e = seco::launch_bwd_sm100(g, tq, tdo, tk, tv, tdq, tdkv, o, d_o, lse, relay_scale, grad_scale, dkv, dq, dk_own, dv_own,
                              ws_dqacc, ws_D, cs, &launches);

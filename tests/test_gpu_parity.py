@@ -71,6 +71,8 @@ BF16_CASES = [
     dict(hq=4, hkv=1, seq=1024, d=128, c=256),    # several tiles per chunk, G=4
     dict(hq=3, hkv=1, seq=768, d=128, c=384),     # odd G -> one head per CTA (NH=1), 3 tiles / chunk
     dict(hq=2, hkv=2, seq=512, d=128, c=256),     # MHA (G=1)
+    dict(hq=8, hkv=2, seq=512, d=64, c=128),      # d = 64 (zero-padded 128-wide tiles)
+    dict(hq=3, hkv=1, seq=768, d=64, c=384),      # d = 64, NH=1
 ]
 
 
@@ -139,10 +141,10 @@ def test_bf16_chunk_calls_compose():
     assert float(layer.dkv[:, :, 3 * c:].abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("j", [2, 3])
-def test_bf16_forward_split_kv(j):
+@pytest.mark.parametrize("j,d", [(2, 128), (3, 128), (3, 64)])
+def test_bf16_forward_split_kv(j, d):
     """Long chunks: the forward splits each query tile's key range and merges partials (a9)."""
-    hq, hkv, seq, d, c = 8, 2, 4096, 128, 1024      # 32 units < 148 SMs: the forward splits
+    hq, hkv, seq, c = 8, 2, 4096, 1024              # 32 units < 148 SMs: the forward splits
     x = inputs(hq, hkv, seq, d, seed=7, peaky=(j == 3))
     q, k, v, do = upload(x, torch.bfloat16)
     layer = _layer(hq, hkv, d, seq, c, torch.bfloat16)
