@@ -143,6 +143,21 @@ def cpu_oracle_sample(cfg, steps=1):
     return fl / dt / 1e12, dt, desc, threads
 
 
+def config_block(args, cfg, world, sel=None, gamma=None):
+    """The `config` object of the JSON line -- identical for both arms."""
+    from paper_2505_16710_b200.parallel import LORA_PARAMS_LLAMA3_8B_R8
+    hq, hkv, d, seq, c = cfg["hq"], cfg["hkv"], cfg["d"], cfg["seq"], cfg["chunk"]
+    k = seq // c
+    n_seq = world if (args.shard == "batch" or world == 1) else 1
+    return {"workload": f"{args.config}: Llama-3-8B attention shape, seq {seq}, chunk {c}, {args.mode}"
+                        + (f" t={args.t} of {k} (I={sel}, gamma={gamma})" if sel is not None else ""),
+            "hq": hq, "hkv": hkv, "d": d, "seq_len": seq, "chunk": c, "num_chunks": k,
+            "mode": args.mode, "sequences_per_step": n_seq, "deterministic": args.deterministic,
+            "parallelism": f"{args.shard}{world}" if world > 1 else "single",
+            "allreduce_bytes_per_step": (LORA_PARAMS_LLAMA3_8B_R8 * 4 if args.allreduce else 0),
+            "l2_policy": "inputs larger than L2 (Q,dO 256 MiB, K,V 64 MiB each, dKV 256 MiB per rank)"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -160,7 +175,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
             "higher_is_better": True, "scaling": "strong" if (args.shard == "heads" and world > 1) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} SeCO, bounded host sample", **cfg},
+            "config": config_block(args, cfg, world),
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -183,10 +198,19 @@ def main():
     from paper_2505_16710_b200.step import ChunkedAttention
     from paper_2505_16710_b200 import ops, flops as FL
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # SECO_BENCH_SHARED_GPU=1 is a plumbing check only (never a measurement): every rank uses
+    # cuda:0 and gloo carries the barrier / max-over-ranks, so the N > 1 code path can be
+    # exercised on a one-GPU box (ranks share nothing on the data path).
+    shared = os.environ.get("SECO_BENCH_SHARED_GPU") == "1"
+    gpu_index = 0 if shared else local_rank
+    torch.cuda.set_device(gpu_index)
+    dev = torch.device("cuda", gpu_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    coll_dev = torch.device("cpu") if shared else dev
     cfg = dict(CONFIGS[args.config])
     hq, hkv, d, seq, c = cfg["hq"], cfg["hkv"], cfg["d"], cfg["seq"], cfg["chunk"]
     from paper_2505_16710_b200.parallel import (LORA_PARAMS_LLAMA3_8B_R8, allreduce_grad_bucket, head_shard,
@@ -244,7 +268,7 @@ def main():
     launches = 0
     mem_before = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(gpu_index)
     with clk:
         t_start.record(stream)
         for s in range(args.steps):
@@ -275,7 +299,7 @@ def main():
                 t_f += dt
             else:
                 t_b += dt
-    ms = max_over_ranks(ms_local, dev)
+    ms = max_over_ranks(ms_local, coll_dev)
     ms_per_step = ms / args.steps
 
     step_flops_rank = FL.seco_step_flops(hq_r, d, seq, c) if sel is None else \
@@ -365,7 +389,7 @@ def main():
             s_in.wait_event(drained[args.steps % 2])
         e1.record(s_in)
         torch.cuda.synchronize()
-        ems = max_over_ranks(e0.elapsed_time(e1), dev)
+        ems = max_over_ranks(e0.elapsed_time(e1), coll_dev)
         e2e = {"value": total_flops / (ems / args.steps * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": ems / args.steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "pinned host Q,K,V,dO -> device (copy stream); SeCO/SpaCO step via C ABI; dQ, dKV -> "
@@ -384,14 +408,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if (args.shard == "heads" and world > 1) else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.config}: Llama-3-8B attention shape, seq {seq}, chunk {c}, "
-                                   f"{args.mode}" + (f" t={args.t} of {k} (I={sel}, gamma={gamma})"
-                                                     if sel is not None else ""),
-                       "hq": hq, "hkv": hkv, "d": d, "seq_len": seq, "chunk": c, "num_chunks": k,
-                       "mode": args.mode, "sequences_per_step": n_seq, "deterministic": args.deterministic,
-                       "parallelism": f"{args.shard}{world}" if world > 1 else "single",
-                       "allreduce_bytes_per_step": (LORA_PARAMS_LLAMA3_8B_R8 * 4 if args.allreduce else 0),
-                       "l2_policy": "inputs larger than L2 (Q,dO 256 MiB, K,V 64 MiB each, dKV 256 MiB per rank)"},
+            "config": config_block(args, cfg, world, sel, gamma),
             "tokens_per_s": tokens / (ms_per_step * 1e-3),
             "step_tflop": total_flops / 1e12,
             "roofline": roofline, "kernels": kern, "memory": memory,
