@@ -17,10 +17,11 @@ Modules
   chunkwise   O5 SeCO step (Alg. 1), O6 SpaCO step (Alg. 2)
   sampler     O8 splitmix64 index sampler and compensation / seed scales
   expectation O7 exact closed forms of E[SpaCO gradient] + subset enumeration
+  multilayer  O9 L-layer RoPE + LoRA attention stack: loss and exact full-sequence gradients
 
 Every function is pinned by a ``-m "not gpu"`` test in ``tests/test_oracle_*.py``
 against something other than itself (torch SDPA + autograd on CPU fp64, central
 finite differences, closed-form special cases, invariants, published splitmix64
 values, exhaustive subset enumeration).  No function is "parity unpinned".
 """
-from . import attention, chunkwise, sampler, expectation  # noqa: F401
+from . import attention, chunkwise, sampler, expectation, multilayer  # noqa: F401

@@ -75,3 +75,39 @@ def make_inputs(hq: int, hkv: int, seq: int, d: int, seed: int = 0,
                           bf16_bits_to_f32(dob), qb, kb, vb, dob)
     z = np.zeros(0, np.uint16)
     return AttnInputs(q, k, v, do, z, z, z, z)
+
+
+@dataclass
+class StackInputs:
+    """Inputs of the L-layer stack (oracle/multilayer.py, paper_2505_16710_b200/model.py):
+    x0 [S][Hd] token states entering layer 0, G [S][Hd] the loss cotangent at the top,
+    layers[l] = {W_p, A_p, B_p for p in q, k, v, o} ([in][out]).  All float64 arrays whose
+    values are exactly representable in the requested dtype (bf16 or float32)."""
+    x0: np.ndarray
+    G: np.ndarray
+    layers: list
+
+
+def make_stack_inputs(L: int, hd: int, hq: int, hkv: int, d: int, r: int, seq: int, seed: int = 0,
+                      bf16: bool = False, w_scale: float = 1.0, lora_scale: float = 0.5) -> StackInputs:
+    """Seeded parameters and inputs.  Base weights ~ N(0, w_scale^2 / fan_in); LoRA A, B ~
+    N(0, lora_scale^2 / fan_in), B non-zero so that every gradient is non-trivial; x0, G ~
+    N(0, 1).  Values are rounded to bf16 (RNE) or to float32."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    rnd = round_to_bf16 if bf16 else (lambda a: np.asarray(a, np.float32))
+
+    def draw(shape, scale):
+        return rnd((rng.standard_normal(shape) * scale).astype(np.float32)).astype(np.float64)
+
+    dims = {"q": (hd, hq * d), "k": (hd, hkv * d), "v": (hd, hkv * d), "o": (hq * d, hd)}
+    layers = []
+    for _ in range(L):
+        p = {}
+        for n, (i, o) in dims.items():
+            p["W" + n] = draw((i, o), w_scale / np.sqrt(i))
+            p["A" + n] = draw((i, r), lora_scale / np.sqrt(i))
+            p["B" + n] = draw((r, o), lora_scale / np.sqrt(r))
+        layers.append(p)
+    x0 = draw((seq, hd), 1.0)
+    G = draw((seq, hd), 1.0)
+    return StackInputs(x0, G, layers)
