@@ -1,0 +1,110 @@
+"""Multi-layer integration on the GPU: an L-layer RoPE + LoRA attention
+stack trained chunk-wise (paper_2505_16710_b200/model.py, attention through the C ABI)
+against the exact full-sequence gradients of oracle/multilayer.py (O9):
+  * SeCO = full-sequence backward (SeCO is exact), fp32 debug kernels and bf16;
+  * SpaCO with independent Bernoulli(rho) selection and s = gamma = 1/rho is unbiased at any
+    depth (reading Z7): the probability-weighted sum over all 2^k selections equals SeCO --
+    the multi-hop chains of Eq. 3 across 2 layers included;
+  * SpaCO selecting every chunk with gamma = s = 1 reproduces SeCO bit for bit
+    (deterministic mode)."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import multilayer as OM
+from synth import make_stack_inputs
+from tests.gpu_util import err
+
+pytestmark = pytest.mark.gpu
+
+
+def _stack(inp, hq, hkv, d, S, c, dtype, deterministic=False):
+    from paper_2505_16710_b200.model import ChunkedLoRAStack
+    return ChunkedLoRAStack(inp.layers, hq, hkv, d, S, c, dtype=dtype, deterministic=deterministic)
+
+
+def _inputs(inp, dtype):
+    return torch.tensor(inp.x0, dtype=dtype), torch.tensor(inp.G, dtype=torch.float32)
+
+
+def _check(model, dx0, inp, hq, hkv, d, tol):
+    grads, rdx0 = OM.stack_grads(inp.x0, inp.layers, inp.G, hq, hkv, d)
+    got = model.lora_grads()
+    worst = 0.0
+    for li, g in enumerate(grads):
+        for n in OM.PROJ:
+            for ab in "AB":
+                e = err(got[(li, ab + n)], g[ab + n])
+                worst = max(worst, e)
+                assert e <= tol, (li, ab + n, e)
+    e = err(dx0.double().cpu().numpy(), rdx0)
+    assert e <= tol, ("dx0", e)
+    return max(worst, e)
+
+
+@pytest.fixture(autouse=True)
+def _no_tf32():
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    yield
+    torch.backends.cuda.matmul.allow_tf32 = old
+
+
+@pytest.mark.parametrize("L,hq,hkv,d,hd,S,c", [(2, 4, 2, 16, 32, 64, 16), (3, 2, 1, 32, 48, 96, 32)])
+def test_fp32_seco_stack_matches_full_gradient(L, hq, hkv, d, hd, S, c):
+    inp = make_stack_inputs(L, hd, hq, hkv, d, 4, S, seed=L)
+    model = _stack(inp, hq, hkv, d, S, c, torch.float32)
+    x0, G = _inputs(inp, torch.float32)
+    dx0 = model.step(x0, G)
+    torch.cuda.synchronize()
+    _check(model, dx0, inp, hq, hkv, d, 1e-4)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_bf16_seco_stack_matches_full_gradient(d):
+    L, hq, hkv, hd, S, c = 2, 4, 2, 128, 512, 128
+    inp = make_stack_inputs(L, hd, hq, hkv, d, 8, S, seed=11, bf16=True)
+    model = _stack(inp, hq, hkv, d, S, c, torch.bfloat16)
+    x0, G = _inputs(inp, torch.bfloat16)
+    dx0 = model.step(x0, G)
+    torch.cuda.synchronize()
+    _check(model, dx0, inp, hq, hkv, d, 3e-2)    # measured worst 1.1e-2 (two bf16 layers)
+
+
+def test_fp32_spaco_bernoulli_unbiased_across_layers():
+    L, hq, hkv, d, hd, S, c = 2, 2, 1, 16, 24, 64, 16
+    k, rho = S // c, 0.5
+    inp = make_stack_inputs(L, hd, hq, hkv, d, 3, S, seed=5)
+    model = _stack(inp, hq, hkv, d, S, c, torch.float32)
+    x0, G = _inputs(inp, torch.float32)
+    model.step(x0, G)
+    seco = model.lora_grads()
+    mean = {key: np.zeros_like(v) for key, v in seco.items()}
+    for n in range(k + 1):
+        for sel in itertools.combinations(range(k), n):
+            w = rho ** n * (1 - rho) ** (k - n)
+            if n == 0:
+                continue                       # no chunk selected: zero gradient
+            model.step(x0, G, selected=sel, relay_scale=1 / rho, seed_scale=1 / rho)
+            for key, v in model.lora_grads().items():
+                mean[key] += w * v
+    torch.cuda.synchronize()
+    for key in seco:
+        assert err(mean[key], seco[key]) <= 1e-4, key
+
+
+def test_bf16_spaco_all_chunks_is_seco():
+    L, hq, hkv, d, hd, S, c = 2, 4, 2, 64, 128, 512, 128
+    inp = make_stack_inputs(L, hd, hq, hkv, d, 8, S, seed=2, bf16=True)
+    model = _stack(inp, hq, hkv, d, S, c, torch.bfloat16, deterministic=True)
+    x0, G = _inputs(inp, torch.bfloat16)
+    a = model.step(x0, G).clone()
+    ga = model.lora_grads()
+    b = model.step(x0, G, selected=list(range(S // c)), relay_scale=1.0, seed_scale=1.0)
+    gb = model.lora_grads()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    for key in ga:
+        assert np.array_equal(ga[key], gb[key]), key
