@@ -136,6 +136,33 @@ seco_status spaco_sample_and_scale(int32_t k, int32_t t, uint64_t seed, float ca
                                    int32_t* idx_out, int32_t* n_out,
                                    float* relay_scale_out, float* seed_scale_out);
 
+/* ---- LoRA gradient accumulation ----------------------------------
+ * For one LoRA-adapted projection Y = X W + (X A) B (LoRA on q, k, v, o of every
+ * layer) and the cotangent dY of one chunk's rows:
+ *   u = dY B^T   -> u_out [rows][rank] float32 (the caller forms dX = dY W^T + u A^T)
+ *   dA += X^T u        [n_in][rank]   float32 accumulator
+ *   dB += (X A)^T dY   [rank][n_out]  float32 accumulator
+ * The accumulators are caller-owned (zeroed by the caller once per step) and sum the
+ * chunks of a step in fp32; a layer's pair is final after its last chunk -- the
+ * moment its all-reduce bucket can be sent (paper_2505_16710_b200/parallel.py).
+ * Layouts: X [rows][n_in], dY [rows][n_out] row-major, row strides ldx, ldy in
+ * elements (>= n_in, n_out); A [n_in][rank] and B [rank][n_out] dense, all of
+ * `dtype` (SECO_BF16 or SECO_FP32_DEBUG).  Fixed summation order: deterministic.
+ * Errors: SECO_ERR_ARG (null pointer, non-positive size, short stride, workspace
+ * too small, unknown dtype), SECO_ERR_UNSUPPORTED (rank not in {1, 2, 4, 8, 16}). */
+typedef struct {
+  int32_t rows, n_in, n_out, rank;
+  seco_dtype dtype;
+  int64_t ldx, ldy;
+} seco_lora_shape;
+
+/* Bytes of device workspace seco_lora_grad needs. */
+size_t seco_lora_workspace_size(const seco_lora_shape* shape);
+
+seco_status seco_lora_grad(const seco_lora_shape* shape, const void* x, const void* dy, const void* a,
+                           const void* b, float* da, float* db, float* u_out, void* ws, size_t ws_bytes,
+                           seco_stream_t stream);
+
 /* Static string for a status code (never NULL). */
 const char* seco_status_string(seco_status status);
 

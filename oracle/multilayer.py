@@ -108,3 +108,13 @@ def stack_grads(x0, layers, G, hq, hkv, d, base=10000.0):
             g["B" + n] = p["A" + n].T @ dW[n]
         grads[li] = g
     return grads, dx
+
+
+def lora_grads(x, dy, A, B):
+    """the LoRA gradients of one projection Y = X W + (X A) B (LoRA) for the
+    cotangent dY, through the merged-weight gradient dW' = X^T dY of O9 (stack_grads):
+    dA = dW' B^T, dB = A^T dW'; also u = dY B^T (what dX = dY W^T + u A^T needs).
+    Returns (dA [n_in][r], dB [r][n_out], u [rows][r])."""
+    x, dy, A, B = (np.asarray(a, np.float64) for a in (x, dy, A, B))
+    dW = x.T @ dy
+    return dW @ B.T, A.T @ dW, dy @ B.T

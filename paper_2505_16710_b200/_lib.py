@@ -14,6 +14,7 @@ SECO_BF16, SECO_FP32_DEBUG = 0, 1
 SPACO_PAPER, SPACO_HT, SPACO_BERNOULLI = 0, 1, 2
 
 EXPORTS = ("seco_workspace_size", "seco_chunk_forward", "seco_chunk_backward", "spaco_sample_and_scale",
+           "seco_lora_workspace_size", "seco_lora_grad",
            "seco_status_string", "seco_last_error", "seco_last_launch_count")
 
 
@@ -27,6 +28,11 @@ class SecoShape(ctypes.Structure):
 
 
 SECO_FLAG_DETERMINISTIC = 1
+
+
+class LoraShape(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int32), ("n_in", ctypes.c_int32), ("n_out", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("dtype", ctypes.c_int32), ("ldx", ctypes.c_int64), ("ldy", ctypes.c_int64)]
 
 
 class SecoError(RuntimeError):
@@ -56,6 +62,10 @@ def load():
     lib.seco_chunk_backward.restype = i32
     lib.spaco_sample_and_scale.argtypes = [i32, i32, ctypes.c_uint64, f32, i32, P(i32), P(i32), P(f32), P(f32)]
     lib.spaco_sample_and_scale.restype = i32
+    lib.seco_lora_workspace_size.argtypes = [P(LoraShape)]
+    lib.seco_lora_workspace_size.restype = sz
+    lib.seco_lora_grad.argtypes = [P(LoraShape), vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.seco_lora_grad.restype = i32
     lib.seco_status_string.argtypes = [i32]
     lib.seco_status_string.restype = ctypes.c_char_p
     lib.seco_last_error.argtypes = []

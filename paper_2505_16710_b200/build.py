@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
           "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
-SOURCES = ["seco_api.cpp", "aux_kernels.cu", "fwd_sm100.cu", "bwd_sm100.cu"]
+SOURCES = ["seco_api.cpp", "aux_kernels.cu", "fwd_sm100.cu", "bwd_sm100.cu", "lora.cu"]
 HEADERS = [os.path.join(ROOT, "include", "seco.h"), os.path.join(CSRC, "common.cuh"),
            os.path.join(CSRC, "kernels.h")]
 

@@ -36,4 +36,14 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              void* dk_own, void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st,
                              int* launches);
 
+// ---- LoRA gradient accumulation (lora.cu) ------------------------------------------------
+struct LoraGeom {
+  int rows, n_in, n_out, rank;
+  int64_t ldx, ldy;
+};
+size_t lora_ws_floats(const LoraGeom& g);
+cudaError_t launch_lora_grad(const LoraGeom& g, bool bf16, const void* x, const void* dy, const void* a,
+                             const void* b, float* da, float* db, float* u, float* ws, cudaStream_t st,
+                             int* launches);
+
 }  // namespace seco

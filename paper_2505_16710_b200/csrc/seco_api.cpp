@@ -252,6 +252,39 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
   return SECO_OK;
 }
 
+static bool lora_geom(const seco_lora_shape* s, seco::LoraGeom* g) {
+  if (!s || s->rows <= 0 || s->n_in <= 0 || s->n_out <= 0 || s->rank <= 0) return false;
+  g->rows = s->rows; g->n_in = s->n_in; g->n_out = s->n_out; g->rank = s->rank;
+  g->ldx = s->ldx; g->ldy = s->ldy;
+  return true;
+}
+
+size_t seco_lora_workspace_size(const seco_lora_shape* s) {
+  seco::LoraGeom g;
+  if (!lora_geom(s, &g)) return 0;
+  return seco::lora_ws_floats(g) * sizeof(float);
+}
+
+seco_status seco_lora_grad(const seco_lora_shape* s, const void* x, const void* dy, const void* a, const void* b,
+                           float* da, float* db, float* u_out, void* ws, size_t ws_bytes, seco_stream_t stream) {
+  g_launches = 0;
+  seco::LoraGeom g;
+  if (!lora_geom(s, &g)) return fail(SECO_ERR_ARG, "lora: NULL shape or non-positive size");
+  if (!x || !dy || !a || !b || !da || !db || !u_out || !ws) return fail(SECO_ERR_ARG, "lora: NULL pointer");
+  if (s->ldx < s->n_in || s->ldy < s->n_out) return fail(SECO_ERR_ARG, "lora: row stride shorter than the row");
+  if (s->dtype != SECO_BF16 && s->dtype != SECO_FP32_DEBUG) return fail(SECO_ERR_ARG, "lora: unknown dtype");
+  if (s->rank != 1 && s->rank != 2 && s->rank != 4 && s->rank != 8 && s->rank != 16)
+    return fail(SECO_ERR_UNSUPPORTED, "lora: rank must be 1, 2, 4, 8 or 16 (got %d)", s->rank);
+  if (ws_bytes < seco_lora_workspace_size(s)) return fail(SECO_ERR_ARG, "lora: workspace too small");
+  int launches = 0;
+  cudaError_t e = seco::launch_lora_grad(g, s->dtype == SECO_BF16, x, dy, a, b, da, db, u_out,
+                                         reinterpret_cast<float*>(ws), reinterpret_cast<cudaStream_t>(stream),
+                                         &launches);
+  if (e != cudaSuccess) return cuda_fail(e, "lora_grad");
+  g_launches = launches;
+  return SECO_OK;
+}
+
 seco_status spaco_sample_and_scale(int32_t k, int32_t t, uint64_t seed, float cap, spaco_mode mode,
                                    int32_t* idx_out, int32_t* n_out, float* relay_scale_out,
                                    float* seed_scale_out) {

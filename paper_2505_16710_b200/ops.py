@@ -8,7 +8,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import SecoShape, check, load
+from ._lib import LoraShape, SecoShape, check, load
 
 _DTYPES = {torch.bfloat16: _lib.SECO_BF16, torch.float32: _lib.SECO_FP32_DEBUG}
 
@@ -82,3 +82,24 @@ def spaco_sample_and_scale(k: int, t: int, seed: int, cap: float = 2.0, mode: in
 
 def last_launch_count() -> int:
     return int(load().seco_last_launch_count())
+
+
+def lora_shape(x, dy, rank: int) -> LoraShape:
+    """Shape record for X [rows][n_in], dY [rows][n_out] (row-major, unit inner stride)."""
+    if x.dtype not in _DTYPES or dy.dtype != x.dtype:
+        raise TypeError("x / dy must both be bf16 or float32")
+    if x.stride(1) != 1 or dy.stride(1) != 1 or x.shape[0] != dy.shape[0]:
+        raise ValueError("x, dy: [rows][n] with contiguous rows and equal row counts")
+    return LoraShape(x.shape[0], x.shape[1], dy.shape[1], rank, _DTYPES[x.dtype], x.stride(0), dy.stride(0))
+
+
+def seco_lora_workspace_size(shape: LoraShape) -> int:
+    return int(load().seco_lora_workspace_size(ctypes.byref(shape)))
+
+
+def seco_lora_grad(shape: LoraShape, x, dy, a, b, da, db, u_out, ws, stream=None):
+    """dA += X^T (dY B^T), dB += (X A)^T dY (fp32), u_out = dY B^T."""
+    lib = load()
+    wsb = ws.numel() * ws.element_size()
+    check(lib.seco_lora_grad(ctypes.byref(shape), _p(x), _p(dy), _p(a), _p(b), _p(da), _p(db), _p(u_out), _p(ws),
+                             wsb, _stream(stream)), "seco_lora_grad")

@@ -155,3 +155,18 @@ def test_workspace_independent_of_sequence_length(lib):
     assert len(sizes) == 1
     s2 = _shape(chunk=512, q_head_stride=4 * 512 * 128, kv_head_stride=4 * 512 * 128)
     assert lib.seco_workspace_size(ctypes.byref(s2)) == 2 * sizes.pop()
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(rank=3), _lib.SECO_ERR_UNSUPPORTED),
+    (dict(rows=0), _lib.SECO_ERR_ARG),
+    (dict(ldx=10), _lib.SECO_ERR_ARG),
+    (dict(dtype=7), _lib.SECO_ERR_ARG),
+])
+def test_lora_argument_validation(lib, kw, code):
+    d = dict(rows=64, n_in=32, n_out=48, rank=8, dtype=0, ldx=32, ldy=48)
+    d.update(kw)
+    s = _lib.LoraShape(*[d[f] for f, _ in _lib.LoraShape._fields_])
+    dummy = ctypes.c_void_p(1 << 20)
+    r = lib.seco_lora_grad(ctypes.byref(s), dummy, dummy, dummy, dummy, dummy, dummy, dummy, dummy, 1 << 30, None)
+    assert r == code

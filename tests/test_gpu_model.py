@@ -108,3 +108,37 @@ def test_bf16_spaco_all_chunks_is_seco():
     assert torch.equal(a, b)
     for key in ga:
         assert np.array_equal(ga[key], gb[key]), key
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,n_in,n_out,r", [(512, 256, 384, 8), (129, 72, 40, 4), (2048, 1024, 1024, 16)])
+def test_lora_grad_kernel_matches_oracle(dtype, rows, n_in, n_out, r):
+    """seco_lora_grad against oracle.multilayer.lora_grads: dA, dB accumulate (two
+    calls give twice the gradient), u = dY B^T; X is a strided view (padded rows)."""
+    from paper_2505_16710_b200 import ops
+    from synth import round_to_bf16
+    rng = np.random.default_rng(rows + r)
+
+    def draw(shape):
+        a = rng.standard_normal(shape).astype(np.float32)
+        return round_to_bf16(a) if dtype == torch.bfloat16 else a
+
+    x_np, dy_np, a_np, b_np = draw((rows, n_in)), draw((rows, n_out)), draw((n_in, r)), draw((r, n_out))
+    xpad = torch.zeros(rows, n_in + 8, dtype=dtype, device="cuda")
+    xpad[:, :n_in] = torch.from_numpy(x_np).to(dtype)
+    x = xpad[:, :n_in]
+    dy = torch.from_numpy(dy_np).to("cuda", dtype)
+    a = torch.from_numpy(a_np).to("cuda", dtype)
+    b = torch.from_numpy(b_np).to("cuda", dtype)
+    da = torch.zeros(n_in, r, device="cuda")
+    db = torch.zeros(r, n_out, device="cuda")
+    u = torch.empty(rows, r, device="cuda")
+    shape = ops.lora_shape(x, dy, r)
+    ws = torch.empty(ops.seco_lora_workspace_size(shape) // 4, device="cuda")
+    for _ in range(2):
+        ops.seco_lora_grad(shape, x, dy, a, b, da, db, u, ws)
+    torch.cuda.synchronize()
+    rdA, rdB, ru = (np.asarray(t) for t in __import__("oracle").multilayer.lora_grads(x_np, dy_np, a_np, b_np))
+    assert err(da.cpu().numpy(), 2 * rdA) <= 1e-5
+    assert err(db.cpu().numpy(), 2 * rdB) <= 1e-5
+    assert err(u.cpu().numpy(), ru) <= 1e-5

@@ -103,3 +103,19 @@ def test_single_layer_without_lora_is_one_attention():
     o, _ = OA.full_attn_fwd(q, k, v)
     want = x + o.transpose(1, 0, 2).reshape(S, hq * d) @ p["Wo"]
     assert np.abs(OM.stack_forward(x, [p], hq, hkv, d) - want).max() < 1e-12
+
+
+def test_lora_grads_match_torch_autograd():
+    rng = np.random.default_rng(4)
+    rows, n_in, n_out, r = 37, 24, 20, 4
+    x, dy = rng.standard_normal((rows, n_in)), rng.standard_normal((rows, n_out))
+    A, B, W = rng.standard_normal((n_in, r)), rng.standard_normal((r, n_out)), rng.standard_normal((n_in, n_out))
+    dA, dB, u = OM.lora_grads(x, dy, A, B)
+    tx = torch.tensor(x, requires_grad=True)
+    tA, tB = torch.tensor(A, requires_grad=True), torch.tensor(B, requires_grad=True)
+    y = tx @ torch.tensor(W) + (tx @ tA) @ tB
+    (y * torch.tensor(dy)).sum().backward()
+    assert np.abs(dA - tA.grad.numpy()).max() < 1e-10
+    assert np.abs(dB - tB.grad.numpy()).max() < 1e-10
+    # dX = dY W^T + u A^T
+    assert np.abs(dy @ W.T + u @ A.T - tx.grad.numpy()).max() < 1e-10
