@@ -12,8 +12,12 @@ slots < j, and when chunk i is processed later (descending order) the relayed sl
 carries it through W'_k, W'_v into x_i of layer l and on into layer l-1 -- the multi-hop
 chains of Eq. 3.
 
-Torch does the projections (library GEMMs, cuBLAS) and the autograd bookkeeping; every
-attention forward / backward is a libseco.so call through the C ABI (ops.py).  The KV cache
+Torch does the base projections (library GEMMs, cuBLAS) and the autograd bookkeeping; every
+attention forward / backward and every LoRA-gradient accumulation (SURVEY f2:
+`seco_lora_grad`, fp32 per-layer buckets summed over the chunks of a step) is a libseco.so
+call through the C ABI (ops.py).  A layer's bucket is final once the step's last chunk has
+passed through it, and is handed to a `LayerBucketReducer` right then, so with several
+data-parallel ranks its all_reduce overlaps the backward of the layers below.  The KV cache
 is kept sequence-major ([S][Hkv][d], the projection output layout) and Q/O/dO/dQ of a chunk
 are [c][Hq][d] -- the ABI's strided layouts, no transposes.
 """
@@ -22,6 +26,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib, ops
+from .parallel import LayerBucketReducer
 
 _DT = {torch.bfloat16: _lib.SECO_BF16, torch.float32: _lib.SECO_FP32_DEBUG}
 PROJ = ("q", "k", "v", "o")
@@ -71,6 +76,31 @@ class _ChunkAttention(torch.autograd.Function):
         return dq, dk, dv, None, None, None
 
 
+class _LoRAProj(torch.autograd.Function):
+    """Y = X W + (X A) B.  Backward: dA, dB accumulate in fp32 into the layer's bucket via
+    seco_lora_grad (which also returns u = dY B^T); dX = dY W^T + u A^T (cuBLAS)."""
+
+    @staticmethod
+    def forward(ctx, x, W, A, B, model, li, name):
+        ctx.save_for_backward(x, W, A, B)
+        ctx.model, ctx.li, ctx.name = model, li, name
+        return x @ W + (x @ A) @ B
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, W, A, B = ctx.saved_tensors
+        m, li, name = ctx.model, ctx.li, ctx.name
+        dy = dy.contiguous()
+        u = torch.empty(x.shape[0], A.shape[1], dtype=torch.float32, device=x.device)
+        shape = ops.lora_shape(x, dy, A.shape[1])
+        ws = m._lora_ws(ops.seco_lora_workspace_size(shape))
+        dA, dB = m.lora_views[li]["A" + name], m.lora_views[li]["B" + name]
+        ops.seco_lora_grad(shape, x, dy, A, B, dA, dB, u, ws)
+        dx = dy @ W.t() + u.to(x.dtype) @ A.t()
+        m._lora_done(li)
+        return dx, None, None, None, None, None, None
+
+
 class ChunkedLoRAStack:
     """L attention blocks; `params[l]` holds W_p (frozen) and A_p, B_p (trainable leaves)."""
 
@@ -85,10 +115,25 @@ class ChunkedLoRAStack:
         for p in layers:
             t = {}
             for name, val in p.items():
-                t[name] = torch.as_tensor(val).to(device=self.device, dtype=dtype)
-                if name[0] in "AB":
-                    t[name].requires_grad_(True)
+                t[name] = torch.as_tensor(val).contiguous().to(device=self.device, dtype=dtype)
             self.params.append(t)
+        # fp32 LoRA-gradient bucket per layer (views dA_p [n_in][r], dB_p [r][n_out])
+        self.buckets, self.lora_views = [], []
+        for t in self.params:
+            sizes = [t[ab + n].numel() for n in PROJ for ab in "AB"]
+            bucket = torch.zeros(sum(sizes), dtype=torch.float32, device=self.device)
+            views, off = {}, 0
+            for n in PROJ:
+                for ab in "AB":
+                    num = t[ab + n].numel()
+                    views[ab + n] = bucket[off:off + num].view(t[ab + n].shape)
+                    off += num
+            self.buckets.append(bucket)
+            self.lora_views.append(views)
+        self._ws = torch.empty(0, dtype=torch.float32, device=self.device)
+        self.reducer = LayerBucketReducer()
+        self._final_chunk = False
+        self._pending = [0] * len(self.params)
         self.state = [_LayerState(hq, hkv, d, seq, chunk, dtype, self.device, deterministic) for _ in layers]
         half = d // 2
         inv = rope_base ** (-torch.arange(half, dtype=torch.float64) * 2.0 / d)
@@ -104,15 +149,30 @@ class ChunkedLoRAStack:
         t1, t2 = tf[..., :half], tf[..., half:]
         return torch.cat([t1 * cos - t2 * sin, t2 * cos + t1 * sin], dim=-1).to(self.dtype)
 
-    @staticmethod
-    def _proj(x, p, n):
-        return x @ p["W" + n] + (x @ p["A" + n]) @ p["B" + n]
+    def _proj(self, x, p, n, li=None):
+        if li is None:                                     # no graph (stage 1)
+            return x @ p["W" + n] + (x @ p["A" + n]) @ p["B" + n]
+        return _LoRAProj.apply(x, p["W" + n], p["A" + n], p["B" + n], self, li, n)
+
+    def _lora_ws(self, nbytes):
+        if self._ws.numel() * 4 < nbytes:
+            self._ws = torch.empty((nbytes + 3) // 4, dtype=torch.float32, device=self.device)
+        return self._ws
+
+    def _lora_done(self, li):
+        """Called after each LoRA accumulation; on the step's last chunk, the fourth one of a
+        layer makes its bucket final."""
+        if self._final_chunk:
+            self._pending[li] -= 1
+            if self._pending[li] == 0:
+                self.reducer.layer_final(li, self.buckets[li])
 
     def _block(self, li, x, j, relay, grad):
         p, st, c = self.params[li], self.state[li], self.chunk
-        q = self._rope(self._proj(x, p, "q").view(c, self.hq, self.d), j).contiguous()
-        k = self._rope(self._proj(x, p, "k").view(c, self.hkv, self.d), j).contiguous()
-        v = self._proj(x, p, "v").view(c, self.hkv, self.d).contiguous()
+        gl = li if grad else None
+        q = self._rope(self._proj(x, p, "q", gl).view(c, self.hq, self.d), j).contiguous()
+        k = self._rope(self._proj(x, p, "k", gl).view(c, self.hkv, self.d), j).contiguous()
+        v = self._proj(x, p, "v", gl).view(c, self.hkv, self.d).contiguous()
         st.k_cache[j * c:(j + 1) * c].copy_(k.detach())         # checkpoint m_j of this layer
         st.v_cache[j * c:(j + 1) * c].copy_(v.detach())
         if grad:
@@ -120,7 +180,7 @@ class ChunkedLoRAStack:
         else:
             o = torch.empty_like(q)
             ops.seco_chunk_forward(st.shape, j, q, st.k_cache, st.v_cache, o, st.lse[j], st.ws)
-        return x + self._proj(o.view(c, self.hq * self.d), p, "o")
+        return x + self._proj(o.view(c, self.hq * self.d), p, "o", gl)
 
     # ------------------------------------------------------------------ steps
     def step(self, x0, G, selected=None, relay_scale=1.0, seed_scale=1.0):
@@ -128,16 +188,15 @@ class ChunkedLoRAStack:
         stage 1 forwards every chunk through all layers (no graph); stage 2 rebuilds each
         selected chunk, descending, and backpropagates J_j * seed_scale, relaying through the
         per-layer checkpoint gradients with relay_scale.  Returns dJ/dx0 (zero rows for chunks
-        not processed); LoRA gradients accumulate in params[l]['A*'/'B*'].grad."""
+        not processed); the LoRA gradients (fp32) are in lora_views / buckets, and their
+        all_reduce over data-parallel ranks (if any) has completed when this returns."""
         c = self.chunk
         x0 = x0.to(self.device, self.dtype)
         G = G.to(self.device, torch.float32)
         for st in self.state:
             st.dkv.zero_()
-        for p in self.params:
-            for n in PROJ:
-                for ab in "AB":
-                    p[ab + n].grad = None
+        for b in self.buckets:
+            b.zero_()
         sel = list(range(self.k)) if selected is None else sorted(set(int(i) for i in selected))
         with torch.no_grad():
             for j in range(self.k):                                    # stage 1 (Alg. 1 lines 1-3)
@@ -145,7 +204,9 @@ class ChunkedLoRAStack:
                 for li in range(len(self.params)):
                     x = self._block(li, x, j, 1.0, grad=False)
         dx0 = torch.zeros_like(x0)
+        self._pending = [len(PROJ)] * len(self.params)
         for j in reversed(sel):                                        # stage 2, descending
+            self._final_chunk = j == sel[0]
             xin = x0[j * c:(j + 1) * c].detach().clone().requires_grad_(True)
             x = xin
             for li in range(len(self.params)):
@@ -153,14 +214,11 @@ class ChunkedLoRAStack:
             loss = (x.float() * G[j * c:(j + 1) * c]).sum() * seed_scale
             loss.backward()
             dx0[j * c:(j + 1) * c] = xin.grad
+        self._final_chunk = False
+        self.reducer.wait()
         return dx0
 
     def lora_grads(self):
         """{(layer, 'A'+p / 'B'+p): grad} as float64 CPU arrays (result extraction)."""
-        out = {}
-        for li, p in enumerate(self.params):
-            for n in PROJ:
-                for ab in "AB":
-                    g = p[ab + n].grad
-                    out[(li, ab + n)] = (torch.zeros_like(p[ab + n]) if g is None else g).double().cpu().numpy()
-        return out
+        return {(li, key): v.double().cpu().numpy() for li, views in enumerate(self.lora_views)
+                for key, v in views.items()}

@@ -67,3 +67,27 @@ def allreduce_grad_bucket(bucket):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(bucket, op=dist.ReduceOp.SUM)
     return bucket
+
+
+class LayerBucketReducer:
+    """Per-layer gradient buckets all-reduced as soon as each is final.
+
+    In a SeCO / SpaCO step the last processed chunk (the smallest selected index) finishes the
+    layers top-down, so the all_reduce of layer l's LoRA-gradient bucket (NCCL, async, on its
+    own stream) overlaps the backward of layers l-1 .. 0.  `wait()` joins them at step end.
+    A no-op on one rank or without torch.distributed."""
+
+    def __init__(self):
+        self.handles = []
+        self.sent = []            # layer indices in the order their buckets were sent
+
+    def layer_final(self, layer: int, bucket):
+        import torch.distributed as dist
+        self.sent.append(layer)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            self.handles.append(dist.all_reduce(bucket, op=dist.ReduceOp.SUM, async_op=True))
+
+    def wait(self):
+        for h in self.handles:
+            h.wait()
+        self.handles.clear()

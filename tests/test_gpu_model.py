@@ -60,6 +60,7 @@ def test_fp32_seco_stack_matches_full_gradient(L, hq, hkv, d, hd, S, c):
     dx0 = model.step(x0, G)
     torch.cuda.synchronize()
     _check(model, dx0, inp, hq, hkv, d, 1e-4)
+    assert model.reducer.sent == list(reversed(range(L)))   # buckets final top-down on the last chunk
 
 
 @pytest.mark.parametrize("d", [64, 128])
@@ -76,7 +77,7 @@ def test_bf16_seco_stack_matches_full_gradient(d):
 def test_fp32_spaco_bernoulli_unbiased_across_layers():
     L, hq, hkv, d, hd, S, c = 2, 2, 1, 16, 24, 64, 16
     k, rho = S // c, 0.5
-    inp = make_stack_inputs(L, hd, hq, hkv, d, 3, S, seed=5)
+    inp = make_stack_inputs(L, hd, hq, hkv, d, 4, S, seed=5)
     model = _stack(inp, hq, hkv, d, S, c, torch.float32)
     x0, G = _inputs(inp, torch.float32)
     model.step(x0, G)

@@ -9,8 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2505_16710_b200.parallel import (LORA_PARAMS_LLAMA3_8B_R8, allreduce_grad_bucket, head_shard,
-                                            max_over_ranks)
+from paper_2505_16710_b200.parallel import (LORA_PARAMS_LLAMA3_8B_R8, LayerBucketReducer, allreduce_grad_bucket,
+                                            head_shard, max_over_ranks)
 
 
 def test_head_shard_partition():
@@ -74,3 +74,39 @@ def test_lora_bucket_size():
     """LLaMA3-8B, r=8 on q,k,v,o x 32 layers = 6.82 M params = 27.3 MB fp32."""
     assert LORA_PARAMS_LLAMA3_8B_R8 == 6_815_744
     assert abs(LORA_PARAMS_LLAMA3_8B_R8 * 4 / 1e6 - 27.3) < 0.05
+
+
+def _bucket_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        buckets = [torch.full((100 + l,), float((rank + 1) * (l + 1))) for l in range(3)]
+        red = LayerBucketReducer()
+        for l in (2, 1, 0):                  # top-down, as the last chunk's backward finishes layers
+            red.layer_final(l, buckets[l])
+        red.wait()
+        if rank == 0:
+            out["sent"] = list(red.sent)
+            out["vals"] = [float(b[0]) for b in buckets] + [float(b[-1]) for b in buckets]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_layer_bucket_reducer_gloo():
+    """per-layer buckets are all-reduced (async) in the order layers become final."""
+    world = 2
+    port = 29700 + (os.getpid() % 1000)
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as m:
+        out = m.dict()
+        mp.spawn(_bucket_worker, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
+        assert out["sent"] == [2, 1, 0]
+        assert out["vals"] == [3.0, 6.0, 9.0] * 2
+
+
+def test_layer_bucket_reducer_single_process_noop():
+    red = LayerBucketReducer()
+    b = torch.ones(4)
+    red.layer_final(0, b)
+    red.wait()
+    assert red.sent == [0] and float(b.sum()) == 4.0
