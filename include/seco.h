@@ -147,9 +147,11 @@ seco_status spaco_sample_and_scale(int32_t k, int32_t t, uint64_t seed, float ca
  * moment its all-reduce bucket can be sent (paper_2505_16710_b200/parallel.py).
  * Layouts: X [rows][n_in], dY [rows][n_out] row-major, row strides ldx, ldy in
  * elements (>= n_in, n_out); A [n_in][rank] and B [rank][n_out] dense, all of
- * `dtype` (SECO_BF16 or SECO_FP32_DEBUG).  Fixed summation order: deterministic.
- * Errors: SECO_ERR_ARG (null pointer, non-positive size, short stride, workspace
- * too small, unknown dtype), SECO_ERR_UNSUPPORTED (rank not in {1, 2, 4, 8, 16}). */
+ * `dtype` (SECO_BF16 or SECO_FP32_DEBUG).  n_in, n_out, ldx, ldy must be multiples
+ * of one 16-B vector (8 bf16 / 4 fp32 elements) and x, dy, a, b 16-B aligned.  Fixed
+ * summation order: deterministic.  Errors: SECO_ERR_ARG (null pointer, non-positive
+ * size, short or misaligned stride, workspace too small, unknown dtype),
+ * SECO_ERR_UNSUPPORTED (rank not in {1, 2, 4, 8, 16}). */
 typedef struct {
   int32_t rows, n_in, n_out, rank;
   seco_dtype dtype;

@@ -276,6 +276,11 @@ seco_status seco_lora_grad(const seco_lora_shape* s, const void* x, const void* 
   if (s->rank != 1 && s->rank != 2 && s->rank != 4 && s->rank != 8 && s->rank != 16)
     return fail(SECO_ERR_UNSUPPORTED, "lora: rank must be 1, 2, 4, 8 or 16 (got %d)", s->rank);
   if (ws_bytes < seco_lora_workspace_size(s)) return fail(SECO_ERR_ARG, "lora: workspace too small");
+  const int vec = s->dtype == SECO_BF16 ? 8 : 4;           // 16-B vectors of the row pass
+  if (s->n_in % vec || s->n_out % vec || s->ldx % vec || s->ldy % vec)
+    return fail(SECO_ERR_ARG, "lora: n_in, n_out and row strides must be multiples of %d elements", vec);
+  if (!aligned16(x) || !aligned16(dy)) return fail(SECO_ERR_ARG, "lora: x / dy must be 16-byte aligned");
+  if (!aligned16(a) || !aligned16(b)) return fail(SECO_ERR_ARG, "lora: a / b must be 16-byte aligned");
   int launches = 0;
   cudaError_t e = seco::launch_lora_grad(g, s->dtype == SECO_BF16, x, dy, a, b, da, db, u_out,
                                          reinterpret_cast<float*>(ws), reinterpret_cast<cudaStream_t>(stream),
