@@ -68,7 +68,6 @@ constexpr int kWG = 4;          // compute warpgroups; WG w owns query columns {
 // dQ drain: one thread issues TMA bulk reduce-adds.  (Tried: warps 2-3 moving the tile with
 // ld.shared + red.global.add.v4 to keep the TMA unit free for loads -- 10-15 % slower, the
 // reds clog the MIO queue that the mbarrier traffic of every role also uses.)
-constexpr int kDrainArrivals = 1;
 
 constexpr int R0 = 0, R1 = 128, TM_DK = 256, TM_DV = 384;
 #ifndef SECO_BWD_EMU
@@ -162,9 +161,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
     mbar_init(bar_kv, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_q_full(s), 1);
-      mbar_init(bar_q_empty(s), 1 + kDrainArrivals);   // dK has consumed Q, the dQ drain has read it
+      mbar_init(bar_q_empty(s), 2);     // dK has consumed Q, and the dQ drain has read it
       mbar_init(bar_do_full(s), 1);
-      mbar_init(bar_do_empty(s), 1 + kDrainArrivals);  // dV has consumed dO, the dQ drain has read it
+      mbar_init(bar_do_empty(s), 2);    // dV has consumed dO, and the dQ drain has read it
     }
     mbar_init(bar_s_full, 1);
     mbar_init(bar_ds_half(0), 4 * kWG);  // one elected lane per compute warp
@@ -174,7 +173,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
     mbar_init(bar_stg_half(0), 2 * 4);  // the 8 warps staging dQ rows [64h, 64h + 64)
     mbar_init(bar_stg_half(1), 2 * 4);
     mbar_init(bar_acc, 1);
-    mbar_init(bar_drain_done, kDrainArrivals);
+    mbar_init(bar_drain_done, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {

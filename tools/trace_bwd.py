@@ -35,11 +35,12 @@ torch.cuda.synchronize()
 lib = _lib.load()
 lib.seco_debug_trace_ptr.restype = ctypes.c_void_p
 ptr = lib.seco_debug_trace_ptr()
-CT, SL, IT = 4, 52, 128
+CT, SL, IT = 4, 20, 128
 host = np.zeros((CT, SL, IT), dtype=np.uint64)
 cudart = ctypes.CDLL("libcudart.so.12")
 cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
-assert cudart.cudaMemcpy(host.ctypes.data, ptr, host.nbytes, 2) == 0
+rc = cudart.cudaMemcpy(host.ctypes.data, ptr, host.nbytes, 2)
+assert rc == 0, ("cudaMemcpy", rc)
 t = host.astype(np.int64)
 for cta in range(2):
     n = int((t[cta, 1] > 0).sum())
@@ -71,10 +72,5 @@ for cta in range(2):
         print("     i=%d %6d %6d %6d %6d | dO(i+1) load issued %6d, Q(i+1) issued %6d, dP(i+1) issued %6d" % (
             i, t[cta, 7, i - 1] - b, t[cta, 18, i - 1] - b, 0, t[cta, 8, i - 1] - b,
             t[cta, 19, i + 1] - b, t[cta, 0, i + 1] - b, t[cta, 17, i] - b))
-    print("    per-warp dq_full seen / dq_empty arrive rel. to s_full(i) (warps 4..19)")
-    for i in range(2, 6):
-        b = t[cta, 5, i]
-        print("     i=%d seen  " % i + " ".join("%5d" % (t[cta, 36 + x, i] - b) for x in range(16)))
-        print("     i=%d arrive" % i + " ".join("%5d" % (t[cta, 20 + x, i] - b) for x in range(16)))
     per = np.diff(t[cta, 1, :n])
     print(f"  mean period {per.mean():.0f} cycles over {n} iterations (128 query rows each); MMA ideal 2560")
