@@ -73,6 +73,8 @@ BF16_CASES = [
     dict(hq=2, hkv=2, seq=512, d=128, c=256),     # MHA (G=1)
     dict(hq=8, hkv=2, seq=512, d=64, c=128),      # d = 64 (zero-padded 128-wide tiles)
     dict(hq=3, hkv=1, seq=768, d=64, c=384),      # d = 64, NH=1
+    dict(hq=16, hkv=2, seq=640, d=128, c=128),    # G = 8, 5 chunks of the minimum size
+    dict(hq=6, hkv=3, seq=1536, d=128, c=768),    # odd kv-head count, 6 query tiles per chunk
 ]
 
 
