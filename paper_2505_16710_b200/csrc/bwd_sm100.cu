@@ -487,12 +487,8 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   int* order = g.det ? reinterpret_cast<int*>(ws_D + 2 * (size_t)g.hq * g.c) : nullptr;
   cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.c, relay, st, order);
   if (e != cudaSuccess) return e;
-  static bool attr_set = false;
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(seco_bwd_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd::kBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> attr_done{0};
+  if ((e = ensure_smem_attr(seco_bwd_sm100_kernel, bwd::kBytes, attr_done)) != cudaSuccess) return e;
   bwd::Args a;
   a.c = g.c; a.j = g.j; a.G = g.hq / g.hkv; a.hkv = g.hkv; a.S = g.c * g.k;
   a.scale_log2 = g.scale * 1.4426950408889634f;

@@ -365,11 +365,10 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   using L = fwd::Layout<NH, D, STAGES>;
   static_assert(L::kAlloc <= 232448, "shared memory budget");
   auto kern = seco_fwd_sm100_kernel<NH, D, STAGES>;
-  static bool attr_set = false;  // idempotent; racing setters write the same value
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+  static std::atomic<unsigned long long> attr_done{0};
+  {
+    cudaError_t e = ensure_smem_attr(kern, L::kAlloc, attr_done);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   fwd::Args a;
   a.c = g.c; a.j = g.j; a.hq = g.hq; a.G = g.hq / g.hkv;

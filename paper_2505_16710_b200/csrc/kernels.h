@@ -1,6 +1,7 @@
 // Internal launcher interface between the C-ABI host layer (seco_api.cpp) and the
 // CUDA kernels.  Not part of the public ABI.
 #pragma once
+#include <atomic>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -35,6 +36,20 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              const float* lse, float relay, float gscale, float* dkv, void* dq,
                              void* dk_own, void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st,
                              int* launches);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device), thread-safe:
+// `done` holds one bit per device ordinal (the attribute is per device).
+template <typename Kernel>
+inline cudaError_t ensure_smem_attr(Kernel kern, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // ---- LoRA gradient accumulation (lora.cu) ------------------------------------------------
 struct LoraGeom {
