@@ -38,6 +38,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when th
 #define SECO_FWD_EMU 0
 #endif
 constexpr int kEmuPairs = SECO_FWD_EMU;
+#ifndef SECO_FWD_PDL
+#define SECO_FWD_PDL 1
+#endif
 constexpr int kSMs = 148;                  // B200    // of every 16 column pairs, this many use ex2_emu2
 
 template <int NH, int D, int STAGES>
@@ -122,6 +125,12 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch(&tm_q); tma_prefetch(&tm_k); tma_prefetch(&tm_v); }
+#if SECO_FWD_PDL
+  // Programmatic dependent launch: the next kernel in the stream may start on SMs this grid
+  // leaves idle (its last, partial wave).  Chunk forwards share no data, so a following
+  // forward fills this tail; every other kernel follows a forward with a plain launch.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   if (warp == 2) tmem_alloc<L::kTmemCols>(smem_u32(tmem_slot));
   tc_fence_before();
   __syncthreads();
@@ -353,6 +362,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<L::kTmemCols>(tmem);
+#if SECO_FWD_PDL
+  // do not complete before the kernel this one may have overlapped: keeps "this grid is done"
+  // implying "everything before it in the stream is done" for the plain launches that follow
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 }
 
 cudaError_t launch_fwd_combine(const ChunkGeom& g, int nsplit, const float* part_o, const float* part_lse, void* o,
@@ -407,8 +421,26 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   }
 #endif
   dim3 grid(units * a.nsplit);
-  kern<<<grid, L::kThreads, L::kAlloc, st>>>(tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if (SECO_FWD_PDL && a.nsplit == 1) {
+    // the split path writes fp32 partials into the workspace, which a preceding backward's
+    // final kernel may still be reading: only the unsplit forward may overlap its predecessor
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(L::kThreads);
+    cfg.dynamicSmemBytes = L::kAlloc;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, a);
+    if (e != cudaSuccess) return e;
+  } else {
+    kern<<<grid, L::kThreads, L::kAlloc, st>>>(tq, tk, tv, reinterpret_cast<__nv_bfloat16*>(o), lse, a);
+  }
+  e = cudaGetLastError();
   *launches = 1;
   if (e == cudaSuccess && a.nsplit > 1) {
     e = launch_fwd_combine(g, a.nsplit, a.part_o, a.part_lse, o, lse, st);
