@@ -341,21 +341,41 @@ def main():
 
     # ---------------------------------------------------------------- end to end (host buffers)
     # Every step: H2D of that step's Q, K, V, dO from pinned host memory, the step, D2H of its
-    # dQ and dKV.  Copies run on two copy streams (H2D and D2H use both PCIe directions) and
-    # overlap the neighbouring steps' compute; two device buffer sets (inputs + layer state)
-    # alternate so a step never reads inputs or writes outputs still in flight.
+    # dQ and dKV -- pipelined at chunk granularity.  Host and device tensors are sequence-major
+    # ([S][h][d], the layout a projection produces; the ABI takes its strides), so a chunk is
+    # one contiguous block: K/V/Q of chunk j are copied in stage-1 order and the forward of
+    # chunk j waits only for them; dO arrives in stage-2 (descending) order; dQ_j and dKV slot
+    # j (final once chunk j's backward is done) go back while the earlier chunks compute.
+    # Copies run on two copy streams (both PCIe directions) and also overlap the neighbouring
+    # steps; two device buffer sets alternate so a step never reads inputs or writes outputs
+    # still in flight.
     e2e = None
     if not args.no_e2e:
-        sets = [(q, kc, vc, do), tuple(torch.empty_like(t) for t in (q, kc, vc, do))]
-        layers = [layer, ChunkedAttention(hq_r, hkv_r, d, seq, c, dtype=torch.bfloat16, device=dev,
-                                          deterministic=args.deterministic)]
-        out_dq = [torch.empty(layer.dq.shape, dtype=layer.dq.dtype).pin_memory() for _ in range(2)]
-        out_dkv = [torch.empty(layer.dkv.shape, dtype=layer.dkv.dtype).pin_memory() for _ in range(2)]
-        h2d = sum(t.numel() * t.element_size() for t in pinned)
+        del layer
+        host = [t.transpose(0, 1).contiguous().pin_memory() for t in pinned]      # [S][h][d]
+        sets = [tuple(torch.empty(t.shape, dtype=t.dtype, device=dev) for t in host) for _ in range(2)]
+        layers = [ChunkedAttention(hq_r, hkv_r, d, seq, c, dtype=torch.bfloat16, device=dev,
+                                   deterministic=args.deterministic, layout="shd") for _ in range(2)]
+        out_dq = [torch.empty(seq, hq_r, d, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        out_dkv = [torch.empty(layers[0].dkv.shape, dtype=layers[0].dkv.dtype).pin_memory() for _ in range(2)]
+        h2d = sum(t.numel() * t.element_size() for t in host)
         d2h = out_dq[0].numel() * out_dq[0].element_size() + out_dkv[0].numel() * out_dkv[0].element_size()
         s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         done = [None, None]      # compute-finished event of the last step that used set b
         drained = [None, None]   # D2H-finished event of the last step that used set b
+        stage2 = list(range(k))[::-1] if sel is None else sorted(sel, reverse=True)
+        rest = [j for j in range(k) if j not in stage2]
+
+        def rows(t, j):
+            return t[j * c:(j + 1) * c]
+
+        def d2h_chunk(b, j):
+            rows(out_dq[b], j).copy_(rows(layers[b].dq.transpose(0, 1), j), non_blocking=True)
+            for tt in range(2):
+                for gg in range(hkv_r):
+                    out_dkv[b][tt, gg, j * c:(j + 1) * c].copy_(layers[b].dkv[tt, gg, j * c:(j + 1) * c],
+                                                               non_blocking=True)
+
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
@@ -365,23 +385,44 @@ def main():
         s_out.wait_event(e0)
         for st_i in range(args.steps):
             b = st_i % 2
-            ev_in = torch.cuda.Event()
+            qd, kd, vd, dod = sets[b]
+            lay = layers[b]
+            ev_qkv, ev_do = [torch.cuda.Event() for _ in range(k)], [torch.cuda.Event() for _ in range(k)]
             with torch.cuda.stream(s_in):
                 if done[b] is not None:
                     s_in.wait_event(done[b])
-                for dst, src in zip(sets[b], pinned):
-                    dst.copy_(src, non_blocking=True)
-                ev_in.record(s_in)
-            stream.wait_event(ev_in)
+                for j in range(k):                       # stage-1 order
+                    for dst, src in ((kd, host[1]), (vd, host[2]), (qd, host[0])):
+                        rows(dst, j).copy_(rows(src, j), non_blocking=True)
+                    ev_qkv[j].record(s_in)
+                for j in reversed(range(k)):             # stage-2 order
+                    rows(dod, j).copy_(rows(host[3], j), non_blocking=True)
+                    ev_do[j].record(s_in)
             if drained[b] is not None:
                 stream.wait_event(drained[b])
-            layers[b].step(*sets[b], sel, gamma, sscale, stream=stream)
+            qv, kv, vv, dov = (t.transpose(0, 1) for t in (qd, kd, vd, dod))
+            lay.dkv.zero_()
+            if sel is not None:
+                lay.dq.zero_()
+            for j in range(k):                           # stage 1
+                stream.wait_event(ev_qkv[j])
+                lay.forward_chunk(qv, kv, vv, j)
+            ev_out = {}
+            for j in stage2:                             # stage 2, descending
+                stream.wait_event(ev_do[j])
+                lay.forward_chunk(qv, kv, vv, j)
+                lay.backward_chunk(qv, kv, vv, dov, j, gamma, sscale)
+                ev_out[j] = torch.cuda.Event()
+                ev_out[j].record(stream)
             done[b] = torch.cuda.Event()
             done[b].record(stream)
             with torch.cuda.stream(s_out):
+                for j in stage2:
+                    s_out.wait_event(ev_out[j])
+                    d2h_chunk(b, j)
                 s_out.wait_event(done[b])
-                out_dq[b].copy_(layers[b].dq, non_blocking=True)
-                out_dkv[b].copy_(layers[b].dkv, non_blocking=True)
+                for j in rest:                           # SpaCO: chunks outside the sample
+                    d2h_chunk(b, j)
                 drained[b] = torch.cuda.Event()
                 drained[b].record(s_out)
         s_in.wait_event(drained[(args.steps - 1) % 2])
@@ -392,8 +433,10 @@ def main():
         ems = max_over_ranks(e0.elapsed_time(e1), coll_dev)
         e2e = {"value": total_flops / (ems / args.steps * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": ems / args.steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "pinned host Q,K,V,dO -> device (copy stream); SeCO/SpaCO step via C ABI; dQ, dKV -> "
-                       "pinned host (copy stream); copies of step s overlap compute of steps s-1 / s+1"}
+               "path": "pinned host Q,K,V,dO ([S][h][d]) -> device per chunk in the order the step consumes "
+                       "them (copy stream); SeCO/SpaCO chunk calls via the C ABI, each waiting only for its "
+                       "chunk's inputs; dQ_j, dKV slot j -> pinned host as soon as chunk j's backward is "
+                       "done (copy stream); steps double-buffered"}
         del sets, layers
 
     cpu = None

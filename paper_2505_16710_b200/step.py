@@ -28,7 +28,10 @@ class ChunkedAttention:
     chunk's own K / V (slot j = total own-chunk gradient after chunk j's relay)."""
 
     def __init__(self, hq, hkv, d, seq, chunk, dtype=torch.bfloat16, device="cuda", softmax_scale=0.0,
-                 own_copies=False, deterministic=False):
+                 own_copies=False, deterministic=False, layout="hsd"):
+        """layout "hsd": Q, dO, O, dQ are [hq][S][d] and the KV cache [hkv][S][d] (contiguous);
+        "shd": sequence-major storage [S][h][d] (the projection output layout, where a chunk
+        is one contiguous block), passed and exposed as [h][S][d] views (x.transpose(0, 1))."""
         if seq % chunk:
             raise ValueError("seq must be a multiple of chunk")
         self.hq, self.hkv, self.d, self.seq, self.chunk = hq, hkv, d, seq, chunk
@@ -38,13 +41,22 @@ class ChunkedAttention:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.dtype, self.device = dtype, dev
         dev = self.device
-        self.o = torch.empty(hq, seq, d, dtype=dtype, device=dev)
+        if layout not in ("hsd", "shd"):
+            raise ValueError("layout must be 'hsd' or 'shd'")
+        self.layout = layout
+
+        def buf(h):
+            if layout == "hsd":
+                return torch.empty(h, seq, d, dtype=dtype, device=dev)
+            return torch.empty(seq, h, d, dtype=dtype, device=dev).transpose(0, 1)
+
+        self.o = buf(hq)
         self.lse = torch.empty(self.k, hq, chunk, dtype=torch.float32, device=dev)   # LSE_j dense [hq][c]
-        self.dq = torch.empty(hq, seq, d, dtype=dtype, device=dev)
+        self.dq = buf(hq)
         self.dkv = torch.empty(2, hkv, seq, d, dtype=torch.float32, device=dev)
         self.own = torch.empty(2, hkv, chunk, d, dtype=dtype, device=dev) if own_copies else None
-        probe_q = torch.empty(hq, seq, d, dtype=dtype, device="meta")
-        probe_k = torch.empty(hkv, seq, d, dtype=dtype, device="meta")
+        probe_q = self.o
+        probe_k = buf(hkv)
         self.shape = ops.make_shape(probe_q, probe_k, chunk, softmax_scale, deterministic)
         self.ws = torch.empty(max(ops.seco_workspace_size(self.shape) // 4, 1), dtype=torch.float32, device=dev)
 
@@ -75,8 +87,9 @@ class ChunkedAttention:
         for t, h in ((q, self.hq), (do, self.hq), (k_cache, self.hkv), (v_cache, self.hkv)):
             if t.shape != (h, self.seq, self.d) or t.dtype != self.dtype or t.device != self.device:
                 raise ValueError("input tensor shape / dtype / device mismatch")
-            if not t.is_contiguous():
-                raise ValueError("inputs must be contiguous [heads][seq][d]")
+            want = (self.seq * self.d, self.d, 1) if self.layout == "hsd" else (self.d, h * self.d, 1)
+            if t.stride() != want:
+                raise ValueError(f"inputs must be {self.layout}-laid-out [heads][seq][d] (strides {want})")
 
     def step(self, q, k_cache, v_cache, do, selected=None, relay_scale=1.0, grad_scale=1.0, stream=None):
         """Stage 1: forward of every chunk, ascending (Alg. 1/2 lines 1-3).

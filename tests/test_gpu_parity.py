@@ -226,3 +226,22 @@ def test_bf16_deterministic_mode_bit_reproducible(hq, hkv, seq, c):
         sp.append((layer.dq.clone(), layer.dkv.clone()))
     assert torch.equal(sp[0][0].view(torch.int16), sp[1][0].view(torch.int16))
     assert torch.equal(sp[0][1].view(torch.int32), sp[1][1].view(torch.int32))
+
+
+def test_bf16_chunked_attention_sequence_major_layout():
+    """ChunkedAttention(layout="shd"): sequence-major storage (the bench's end-to-end path)
+    gives the same step as the oracle."""
+    from paper_2505_16710_b200.step import ChunkedAttention
+    hq, hkv, seq, d, c = 8, 2, 1024, 128, 256
+    x = inputs(hq, hkv, seq, d, seed=12)
+    q, k, v, do = (t.transpose(0, 1).contiguous().transpose(0, 1) for t in upload(x, torch.bfloat16))
+    layer = ChunkedAttention(hq, hkv, d, seq, c, layout="shd")
+    layer.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    ref = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (seq // c))
+    assert err(host(layer.o), ref["o"]) <= BF16_TOL
+    assert err(host(layer.dq), ref["dq"]) <= BF16_TOL
+    assert err(host(layer.dkv[0]), ref["dk"]) <= BF16_TOL
+    assert err(host(layer.dkv[1]), ref["dv"]) <= BF16_TOL
+    with pytest.raises(ValueError):
+        layer.seco_step(*upload(x, torch.bfloat16))          # head-major inputs: wrong strides
