@@ -50,17 +50,18 @@ SECO_DEV float warp_sum(float v) {
 }  // namespace lora
 
 // Z[row][k] = sum_i M[row][i] P(i, k) for a [rows][n] matrix M (row stride ldm): P(i, k) =
-// A[i][k] (t = X A) or B[k][i] (u = dY B^T).  A block of 8 warps takes RW rows; its 256
+// A[i][k] (t = X A) or B[k][i] (u = dY B^T).  A block of 4 warps takes RW = 4 rows; its 128
 // lanes stride over 16-B vectors of those rows, each vector's P values coming from L1 (A and
 // B are at most a few hundred KiB), RW x R FMAs per loaded element of P; lane and warp
 // partial sums are reduced through shuffles and smem.
 template <typename T, int R>
-__global__ void __launch_bounds__(256) lora_rows_kernel(const T* __restrict__ m, int64_t ldm,
+__global__ void __launch_bounds__(128) lora_rows_kernel(const T* __restrict__ m, int64_t ldm,
                                                         const T* __restrict__ P, bool p_is_b, int rows, int n,
                                                         float* __restrict__ z) {
   constexpr int VEC = 16 / sizeof(T);           // elements per 16-B vector
-  constexpr int RW = 8;                         // rows per block
-  __shared__ float red[8][RW][R];
+  constexpr int RW = 4;                         // rows per block (register budget: RW x R accumulators)
+  constexpr int NT = 128, NW = NT / 32;         // threads / warps per block
+  __shared__ float red[NW][RW][R];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int r0 = blockIdx.x * RW;
   float acc[RW][R];
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(256) lora_rows_kernel(const T* __restrict__ m,
   for (int q = 0; q < RW; ++q)
 #pragma unroll
     for (int k = 0; k < R; ++k) acc[q][k] = 0.f;
-  for (int i0 = threadIdx.x * VEC; i0 < n; i0 += 256 * VEC) {
+  for (int i0 = threadIdx.x * VEC; i0 < n; i0 += NT * VEC) {
     T xv[RW][VEC];
 #pragma unroll
     for (int q = 0; q < RW; ++q) {
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(256) lora_rows_kernel(const T* __restrict__ m,
     if (r0 + q >= rows) continue;
     float v = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) v += red[w][q][k];
+    for (int w = 0; w < NW; ++w) v += red[w][q][k];
     z[(int64_t)(r0 + q) * R + k] = v;
   }
 }
@@ -221,10 +222,10 @@ static cudaError_t launch_lora_impl(const LoraGeom& g, const void* x, const void
   float* t = ws;
   float* part = ws + (size_t)g.rows * R;
   cudaError_t e;
-  const int blocks = (g.rows + 7) / 8;
-  lora_rows_kernel<T, R><<<blocks, 256, 0, st>>>(X, g.ldx, static_cast<const T*>(a), false, g.rows, g.n_in, t);
+  const int blocks = (g.rows + 3) / 4;
+  lora_rows_kernel<T, R><<<blocks, 128, 0, st>>>(X, g.ldx, static_cast<const T*>(a), false, g.rows, g.n_in, t);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  lora_rows_kernel<T, R><<<blocks, 256, 0, st>>>(dY, g.ldy, static_cast<const T*>(b), true, g.rows, g.n_out, u);
+  lora_rows_kernel<T, R><<<blocks, 128, 0, st>>>(dY, g.ldy, static_cast<const T*>(b), true, g.rows, g.n_out, u);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int nsplit = lora_splits(g);
   const int max_rows = (g.rows + nsplit - 1) / nsplit + 1;
