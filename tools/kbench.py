@@ -17,6 +17,16 @@ hq, hkv, d, S, c = CFG[name]
 k = S // c
 js = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 1, 3, 7, 11, 15]
 R = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+
+    def _sm_mhz():
+        return pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM)
+except Exception:                            # no NVML: report 0
+    def _sm_mhz():
+        return 0
 torch.manual_seed(0)
 q = torch.randn(hq, S, d, device="cuda").bfloat16()
 kc = torch.randn(hkv, S, d, device="cuda").bfloat16()
@@ -38,7 +48,9 @@ for j in js:
         for _ in range(R):
             (L.forward_chunk(q, kc, vc, j) if kind == "fwd" else L.backward_chunk(q, kc, vc, do, j))
         e1.record()
+        mhz = _sm_mhz()                     # sampled while the queued calls still run
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / R
         fl = FL.fwd_flops(hq, d, c, j) if kind == "fwd" else FL.bwd_flops(hq, d, c, j)
-        print(f"{name} j={j:2d} {kind}: {ms * 1e3:8.1f} us  {fl / ms / 1e9:7.1f} TFLOP/s", flush=True)
+        print(f"{name} j={j:2d} {kind}: {ms * 1e3:8.1f} us  {fl / ms / 1e9:7.1f} TFLOP/s  sm {mhz} MHz"
+              f"  {fl / ms / 1e9 / max(mhz, 1) * 1e3:6.1f} TFLOP/s per GHz", flush=True)
