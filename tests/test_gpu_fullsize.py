@@ -115,3 +115,37 @@ def test_memory_ledger_step_allocates_nothing():
     assert len(set(per_call.values())) == 1
     assert ledgers[8]["dkv_fp32_bytes"] == 4 * ledgers[2]["dkv_fp32_bytes"]
     assert ledgers[8]["kv_cache_bytes"] == 4 * ledgers[2]["kv_cache_bytes"]
+
+
+def test_cfg4_rank_shape_seco_sampled_rows_tail_keys_and_invariants():
+    """One rank of BASELINE cfg4 head-sharded over 8 GPUs (4 q heads / 1 kv
+    head, d=128, seq 131072, chunk 4096), the per-rank launch configuration `bench.py --gpus
+    8` times: a sub-wave forward grid (split-KV, row a9) and 4096-row chunks.  Sampled rows
+    one by one; dK / dV of the last 8 keys, which only the last 8 query rows see (exact from
+    those rows alone); and the any-size sums over every key."""
+    from paper_2505_16710_b200.step import ChunkedAttention
+    hq, hkv, d, s, c = 4, 1, 128, 131072, 4096
+    x = make_inputs(hq, hkv, s, d, seed=4)
+    q, k, v, do = upload(x, torch.bfloat16)
+    layer = ChunkedAttention(hq, hkv, d, s, c, dtype=torch.bfloat16)
+    layer.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    o_g, dq_g, lse_g = host(layer.o), host(layer.dq), host(layer.lse_full())
+    rows = [(0, 0), (1, 4095), (2, 4096), (3, 77 * 1000 + 5), (0, s - 4096), (1, s - 1), (3, 31 * 4096 + 4095)]
+    got, ref = {"o": [], "lse": [], "dq": []}, {"o": [], "lse": [], "dq": []}
+    for h, p in rows:
+        qr, dor = x.q[h:h + 1, p:p + 1], x.do[h:h + 1, p:p + 1]
+        o, lse = OA.chunk_fwd(qr, x.k, x.v, p)
+        dq, _, _ = OA.chunk_bwd(qr, x.k, x.v, dor, p)
+        ref["o"].append(o[0, 0]); ref["lse"].append(lse[0, 0]); ref["dq"].append(dq[0, 0])
+        got["o"].append(o_g[h, p]); got["lse"].append(lse_g[h, p]); got["dq"].append(dq_g[h, p])
+    for key in got:
+        assert err(np.array(got[key]), np.array(ref[key])) <= BF16_TOL, key
+    r = 8
+    _, dk_src, dv_src = OA.chunk_bwd(x.q[:, s - r:], x.k, x.v, x.do[:, s - r:], s - r)
+    assert err(host(layer.dk[0, s - r:]), dk_src[0, s - r:]) <= BF16_TOL
+    assert err(host(layer.dv[0, s - r:]), dv_src[0, s - r:]) <= BF16_TOL
+    dk_sum = layer.dk.double().sum(dim=1).cpu().numpy()
+    assert np.abs(dk_sum).max() <= BF16_TOL * layer.dk.double().abs().sum(dim=1).max().item()
+    do_sum = x.do.astype(np.float64).sum(axis=(0, 1))[None]
+    assert err(layer.dv.double().sum(dim=1).cpu().numpy(), do_sum) <= BF16_TOL
