@@ -115,31 +115,45 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def cpu_oracle_sample(cfg, steps=1):
-    """Time the oracle (fp64 NumPy, as it stands) on a bounded sample of the workload:
-    a SeCO step over the first 2 chunks of the sequence for ONE q-head / ONE kv-head.
-    Returns (TFLOP/s, seconds per sample, description, threads)."""
-    import numpy as np
+def oracle_sample_shape(cfg, target_flops):
+    """The bounded oracle sample: whole kv-head groups (G q-heads + their kv head) over the
+    first n chunks of the sequence, the largest such sample whose algorithmic SeCO-step FLOPs
+    stay within target_flops (chunks first, then more groups once the whole sequence fits)."""
+    from paper_2505_16710_b200.flops import seco_step_flops
+    G, c, d, k = cfg["hq"] // cfg["hkv"], cfg["chunk"], cfg["d"], cfg["seq"] // cfg["chunk"]
+    n = 1
+    while n < k and seco_step_flops(G, d, (n + 1) * c, c) <= target_flops:
+        n += 1
+    groups = 1
+    while groups < cfg["hkv"] and seco_step_flops(G * (groups + 1), d, n * c, c) <= target_flops:
+        groups += 1
+    return groups, n
+
+
+def cpu_oracle_sample(cfg, target_flops=0.6e12):
+    """Time the oracle (fp64 NumPy, as it stands) on a bounded sample of the workload
+    (oracle_sample_shape: ~0.6 TFLOP, 10-20 s on 16 host cores for the cpu_baseline key).
+    Returns (TFLOP/s, seconds, description, threads)."""
     from oracle import chunkwise as OC
     from synth import make_inputs
     from paper_2505_16710_b200.flops import seco_step_flops
     c, d = cfg["chunk"], cfg["d"]
-    seq = 2 * c
-    x = make_inputs(1, 1, seq, d, seed=0)
-    fl = seco_step_flops(1, d, seq, c)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        OC.seco_step(x.q, x.k, x.v, x.do, [c, c])
-        times.append(time.perf_counter() - t0)
-    dt = min(times) if steps > 1 else times[0]
+    G = cfg["hq"] // cfg["hkv"]
+    groups, n = oracle_sample_shape(cfg, target_flops)
+    seq = n * c
+    x = make_inputs(G * groups, groups, seq, d, seed=0)
+    fl = seco_step_flops(G * groups, d, seq, c)
+    t0 = time.perf_counter()
+    OC.seco_step(x.q, x.k, x.v, x.do, [c] * n)
+    dt = time.perf_counter() - t0
     try:
         from threadpoolctl import threadpool_info
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
         threads = os.cpu_count()
-    desc = (f"oracle.chunkwise.seco_step fp64 on 1 q-head x 1 kv-head, first {seq} tokens "
-            f"(2 chunks of {c}), d={d}: {fl / 1e9:.1f} GFLOP algorithmic")
+    desc = (f"oracle.chunkwise.seco_step fp64 on {groups} kv-head group(s) ({G * groups} q-heads, {groups} "
+            f"kv-head(s)), first {seq} tokens ({n} chunks of {c}), d={d}: {fl / 1e9:.1f} GFLOP algorithmic "
+            f"(same FLOP model as the GPU arm)")
     return fl / dt / 1e12, dt, desc, threads
 
 
@@ -162,12 +176,14 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
+    # each step a smaller bounded sample (~0.15 TFLOP, a few seconds) so that the whole
+    # --steps K --warmup W run ends within a few minutes
     for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, 1)
+        cpu_oracle_sample(cfg, 0.15e12)
     vals = []
     t_all = 0.0
     for _ in range(args.steps):
-        v, dt, desc, threads = cpu_oracle_sample(cfg, 1)
+        v, dt, desc, threads = cpu_oracle_sample(cfg, 0.15e12)
         vals.append(v)
         t_all += dt
     value = statistics.median(vals)
@@ -460,7 +476,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, desc, threads = cpu_oracle_sample(cfg, 1)
+        v, dt, desc, threads = cpu_oracle_sample(cfg)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": desc,
                "seconds": dt}
 

@@ -33,6 +33,14 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+#include <cstdlib>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
 namespace seco {
 
 #ifdef SECO_TRACE
@@ -78,7 +86,10 @@ constexpr int kEmuPairs = SECO_BWD_EMU;
 
 struct Args {
   int c, j, G, hkv, S;
-  int nsplit;
+  // work list (launch_bwd_sm100 / choose_schedule): blocks [0, n0) take whole units, the next
+  // n1 units are split into f1 query-range pieces each, the remaining units into f2 pieces.
+  // Unit U = (key tile U / hkv, kv head U % hkv); ascending key tiles = descending work.
+  int n0, n1, f1, f2;
   float scale_log2;   // sigma * log2 e
   float dk_scale;     // s * sigma
   float dv_scale;     // s
@@ -137,18 +148,28 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
 #else
 #define TRACE(slot, i) do { } while (0)
 #endif
-  // block -> (key tile u, split s, kv head g); key tiles in ascending order = longest work first
+  // block -> (unit U, piece of f); units in ascending key-tile order = longest work first,
+  // the split (shorter) pieces at the end of the list fill the last wave
   const int bid = blockIdx.x;
-  const int g = bid % a.hkv;
-  const int split = (bid / a.hkv) % a.nsplit;
-  const int u = bid / (a.hkv * a.nsplit);
+  int U, piece, f;
+  if (bid < a.n0) {
+    U = bid; piece = 0; f = 1;
+  } else if (bid < a.n0 + a.n1 * a.f1) {
+    const int r = bid - a.n0;
+    U = a.n0 + r / a.f1; piece = r % a.f1; f = a.f1;
+  } else {
+    const int r = bid - a.n0 - a.n1 * a.f1;
+    U = a.n0 + a.n1 + r / a.f2; piece = r % a.f2; f = a.f2;
+  }
+  const int g = U % a.hkv;
+  const int u = U / a.hkv;
   const int k0 = u * BKV;                                  // first key (absolute position)
   const int nqt = a.c / BQ;
   const int rel = k0 - a.j * a.c;                          // key offset relative to chunk j's first row
   const int qt_min = rel > 0 ? rel / BQ : 0;               // first query tile that sees key k0
   const int n_all = a.G * (nqt - qt_min);
-  const int it0 = (int)((int64_t)split * n_all / a.nsplit);
-  const int it1 = (int)((int64_t)(split + 1) * n_all / a.nsplit);
+  const int it0 = (int)((int64_t)piece * n_all / f);
+  const int it1 = (int)((int64_t)(piece + 1) * n_all / f);
   const int n = it1 - it0;
   // iteration i -> (q-head g*G + hh, query tile qt); each role walks it incrementally
   struct Walk {
@@ -475,6 +496,128 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+namespace {
+// ---- work list for one backward call (host side) ------------------------------------------
+// Units (key tile u of kv-head g) cost G * (query tiles that see the tile) 128x128 blocks: the
+// cache-slot tiles all G c / 128, the diagonal slot's tiles G c / 128 ... G.  One CTA runs per
+// SM and the hardware hands blocks out in index order, so the call's time is that of list
+// scheduling the work list on the SMs.  Whole units first (longest first), then the last units
+// split into f1, then f2 query-range pieces (each piece reduce-adds its own dK/dV share), so the
+// last wave is made of short pieces.  (n0, n1, f1, f2) minimise the simulated makespan with a
+// per-piece overhead of kItemOverhead blocks (prologue, K/V load, dK/dV epilogue);
+// deterministic mode keeps whole units (one owner per dK/dV tile).
+struct Schedule { int n0, n1, f1, f2, grid; };
+
+float item_overhead() {
+  static const float o = [] {
+    const char* e = std::getenv("SECO_BWD_ITEM_OVERHEAD");   // tuning experiments only
+    return e ? (float)std::atof(e) : 3.0f;
+  }();
+  return o;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
+                                                cudaSuccess || n <= 0)
+    return 148;
+  return n;
+}
+
+// makespan of list-scheduling `pieces` (in order) onto P machines whose busy-until times are `t0`
+float list_makespan(std::vector<float> t, const std::vector<float>& pieces) {
+  std::make_heap(t.begin(), t.end(), std::greater<float>());
+  for (float p : pieces) {
+    std::pop_heap(t.begin(), t.end(), std::greater<float>());
+    t.back() += p;
+    std::push_heap(t.begin(), t.end(), std::greater<float>());
+  }
+  return *std::max_element(t.begin(), t.end());
+}
+
+Schedule compute_schedule(int c, int j, int hkv, int G, int P) {
+  const int nqt = c / bwd::BQ, ntiles = (j + 1) * c / bwd::BKV, N = ntiles * hkv;
+  const float o = item_overhead();
+  auto unit_blocks = [&](int U) {
+    const int rel = (U / hkv) * bwd::BKV - j * c;
+    return G * (nqt - (rel > 0 ? rel / bwd::BQ : 0));
+  };
+  auto add_pieces = [&](std::vector<float>& out, int U, int f) {
+    const int nb = unit_blocks(U);
+    for (int p = 0; p < f; ++p) {
+      const int b = (int)((int64_t)(p + 1) * nb / f - (int64_t)p * nb / f);
+      out.push_back(b > 0 ? b + o : 0.25f * o);
+    }
+  };
+  Schedule best{N, 0, 1, 1, N};
+  float best_t;
+  {
+    std::vector<float> all;
+    for (int U = 0; U < N; ++U) add_pieces(all, U, 1);
+    best_t = list_makespan(std::vector<float>(P, 0.f), all);
+  }
+  // split candidates: the last n12 units (steps of 8 units, up to ~2 waves of units); the
+  // busy-until state after the whole-unit prefix is extended incrementally as n12 shrinks
+  constexpr int kStep = 8;
+  const int max12 = std::min(N, 2 * P) / kStep * kStep;
+  static const int kF[][2] = {{2, 2}, {4, 4}, {2, 4}, {2, 8}, {4, 8}};
+  std::vector<float> t(P, 0.f), head, tail;
+  auto push_all = [&](const std::vector<float>& pcs) {
+    for (float p : pcs) {
+      std::pop_heap(t.begin(), t.end(), std::greater<float>());
+      t.back() += p;
+      std::push_heap(t.begin(), t.end(), std::greater<float>());
+    }
+  };
+  std::make_heap(t.begin(), t.end(), std::greater<float>());
+  for (int U = 0; U < N - max12; ++U) add_pieces(head, U, 1);
+  push_all(head);
+  for (int n12 = max12; n12 >= kStep; n12 -= kStep) {
+    const int n0 = N - n12;
+    if (n12 < max12) {
+      head.clear();
+      for (int U = n0 - kStep; U < n0; ++U) add_pieces(head, U, 1);
+      push_all(head);
+    }
+    for (const auto& ff : kF) {
+      for (int n2 = 0; n2 <= n12; n2 += 2 * kStep) {
+        if (ff[0] == ff[1] && n2 > 0) break;   // one split factor: n2 is immaterial
+        tail.clear();
+        for (int U = n0; U < n0 + n12 - n2; ++U) add_pieces(tail, U, ff[0]);
+        for (int U = n0 + n12 - n2; U < N; ++U) add_pieces(tail, U, ff[1]);
+        const float m = list_makespan(t, tail);
+        if (m < best_t * 0.999f) {
+          best_t = m;
+          best = Schedule{n0, n12 - n2, ff[0], ff[1], n0 + (n12 - n2) * ff[0] + n2 * ff[1]};
+        }
+      }
+    }
+  }
+  return best;
+}
+
+Schedule choose_schedule(int c, int j, int hkv, int G, int P) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int>, Schedule> cache;
+  const auto key = std::make_tuple(c, j, hkv, G, P);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const Schedule s = compute_schedule(c, j, hkv, G, P);
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(key, s);
+  return s;
+}
+}  // namespace
+
+extern "C" int32_t seco_debug_bwd_schedule(int32_t c, int32_t j, int32_t hkv, int32_t G, int32_t P, int32_t* out4) {
+  const Schedule s = choose_schedule(c, j, hkv, G, P);
+  out4[0] = s.n0; out4[1] = s.n1; out4[2] = s.f1; out4[3] = s.f2;
+  return s.grid;
+}
+
 cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tdo,
                              const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tdq,
                              const CUtensorMap& tdkv, const void* o, const void* d_o,
@@ -508,13 +651,10 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   }
 #endif
   const int ntiles = (g.j + 1) * g.c / bwd::BKV;
-  // Q-split when the chunk offers fewer key tiles than ~2 waves of SMs; each split keeps
-  // at least one query tile (the shortest, diagonal key tile has G of them).
-  int nsplit = (2 * 148 + ntiles * g.hkv - 1) / (ntiles * g.hkv);
-  if (nsplit > a.G) nsplit = a.G;
-  if (nsplit < 1 || g.det) nsplit = 1;   // deterministic: one owner per dK/dV tile
-  a.nsplit = nsplit;
-  dim3 grid(ntiles * nsplit * g.hkv);
+  const Schedule sc = g.det ? Schedule{ntiles * g.hkv, 0, 1, 1, ntiles * g.hkv}   // one owner per dK/dV tile
+                           : choose_schedule(g.c, g.j, g.hkv, a.G, num_sms());
+  a.n0 = sc.n0; a.n1 = sc.n1; a.f1 = sc.f1; a.f2 = sc.f2;
+  dim3 grid(sc.grid);
   seco_bwd_sm100_kernel<<<grid, bwd::kThreads, bwd::kBytes, st>>>(tq, tdo, tk, tv, tdq, tdkv, a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   e = launch_final_bf16(g, ws_dqacc, dq, dkv, dk_own, dv_own, gscale * g.scale, st);

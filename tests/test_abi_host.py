@@ -170,3 +170,44 @@ def test_lora_argument_validation(lib, kw, code):
     dummy = ctypes.c_void_p(1 << 20)
     r = lib.seco_lora_grad(ctypes.byref(s), dummy, dummy, dummy, dummy, dummy, dummy, dummy, dummy, 1 << 30, None)
     assert r == code
+
+
+def _bwd_work_list(lib, c, j, hkv, G, sms):
+    """Decode the backward work list exactly as seco_bwd_sm100_kernel does (blockIdx ->
+    unit U, piece of f) and return, per unit, the query-iteration ranges of its pieces."""
+    out = (ctypes.c_int32 * 4)()
+    grid = lib.seco_debug_bwd_schedule(c, j, hkv, G, sms, out)
+    n0, n1, f1, f2 = list(out)
+    nqt, ntiles = c // 128, (j + 1) * c // 128
+    ranges = {}
+    for bid in range(grid):
+        if bid < n0:
+            U, piece, f = bid, 0, 1
+        elif bid < n0 + n1 * f1:
+            r = bid - n0
+            U, piece, f = n0 + r // f1, r % f1, f1
+        else:
+            r = bid - n0 - n1 * f1
+            U, piece, f = n0 + n1 + r // f2, r % f2, f2
+        u = U // hkv
+        rel = u * 128 - j * c
+        n_all = G * (nqt - (rel // 128 if rel > 0 else 0))
+        ranges.setdefault(U, []).append((piece * n_all // f, (piece + 1) * n_all // f, n_all))
+    return grid, ntiles * hkv, ranges
+
+
+@pytest.mark.parametrize("c,k,hkv,G", [(2048, 16, 8, 4), (1024, 8, 8, 4), (4096, 32, 1, 4), (1024, 16, 2, 4),
+                                       (256, 5, 3, 2), (128, 4, 1, 1)])
+def test_bwd_work_list_covers_every_block_once(lib, c, k, hkv, G):
+    """The balanced backward work list (whole units, then f1- / f2-way query splits for the
+    last wave): every (key tile, kv head) unit appears, its pieces tile [0, n_all) exactly,
+    and units come in ascending key-tile order (longest work first)."""
+    for j in sorted({0, 1, k // 2, k - 1}):
+        grid, n_units, ranges = _bwd_work_list(lib, c, j, hkv, G, 148)
+        assert sorted(ranges) == list(range(n_units))
+        for U, rs in ranges.items():
+            n_all = rs[0][2]
+            assert rs[0][0] == 0 and rs[-1][1] == n_all
+            for (a0, a1, _), (b0, b1, _) in zip(rs, rs[1:]):
+                assert a1 == b0 and a0 <= a1
+        assert grid >= n_units
