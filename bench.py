@@ -130,9 +130,9 @@ def oracle_sample_shape(cfg, target_flops):
     return groups, n
 
 
-def cpu_oracle_sample(cfg, target_flops=0.6e12):
+def cpu_oracle_sample(cfg, target_flops=1.0e12):
     """Time the oracle (fp64 NumPy, as it stands) on a bounded sample of the workload
-    (oracle_sample_shape: ~0.6 TFLOP, 10-20 s on 16 host cores for the cpu_baseline key).
+    (oracle_sample_shape: <= 1 TFLOP, ~15 s on the 16 host cores of the GPU box, for the cpu_baseline key).
     Returns (TFLOP/s, seconds, description, threads)."""
     from oracle import chunkwise as OC
     from synth import make_inputs

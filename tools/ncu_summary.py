@@ -8,7 +8,7 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
     h = rows[hi]; ki, vi, ui = h.index('Kernel Name'), h.index('Metric Value'), h.index('Metric Unit')
     tot = collections.defaultdict(float); cnt = collections.Counter()
-    scale = {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}
+    scale = {'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1.0, 'us': 1.0, 'msecond': 1e3, 'ms': 1e3}
     for r in rows[hi + 1:]:
         if len(r) <= vi: continue
         name = r[ki].split('(')[0][:70]
