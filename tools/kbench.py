@@ -11,7 +11,7 @@ import torch
 from paper_2505_16710_b200 import flops as FL
 from paper_2505_16710_b200.step import ChunkedAttention
 
-CFG = {"cfg3": (32, 8, 128, 32768, 2048), "cfg2": (32, 8, 128, 8192, 1024)}
+CFG = {"cfg3": (32, 8, 128, 32768, 2048), "cfg2": (32, 8, 128, 8192, 1024), "cfg3p8": (4, 1, 128, 32768, 2048)}
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 hq, hkv, d, S, c = CFG[name]
 k = S // c
