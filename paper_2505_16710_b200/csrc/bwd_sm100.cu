@@ -556,11 +556,12 @@ Schedule compute_schedule(int c, int j, int hkv, int G, int P) {
     for (int U = 0; U < N; ++U) add_pieces(all, U, 1);
     best_t = list_makespan(std::vector<float>(P, 0.f), all);
   }
-  // split candidates: the last n12 units (steps of 8 units, up to ~2 waves of units); the
+  // split candidates: the last n12 units (all of them if the call has <= 2 waves of units,
+  // then in steps of 8); the
   // busy-until state after the whole-unit prefix is extended incrementally as n12 shrinks
-  constexpr int kStep = 8;
-  const int max12 = std::min(N, 2 * P) / kStep * kStep;
-  static const int kF[][2] = {{2, 2}, {4, 4}, {2, 4}, {2, 8}, {4, 8}};
+  const int kStep = 8;
+  const int max12 = std::min(N, 2 * P);
+  static const int kF[][2] = {{2, 2}, {4, 4}, {8, 8}, {2, 4}, {2, 8}, {4, 8}};
   std::vector<float> t(P, 0.f), head, tail;
   auto push_all = [&](const std::vector<float>& pcs) {
     for (float p : pcs) {
@@ -572,7 +573,7 @@ Schedule compute_schedule(int c, int j, int hkv, int G, int P) {
   std::make_heap(t.begin(), t.end(), std::greater<float>());
   for (int U = 0; U < N - max12; ++U) add_pieces(head, U, 1);
   push_all(head);
-  for (int n12 = max12; n12 >= kStep; n12 -= kStep) {
+  for (int n12 = max12; n12 >= 1; n12 -= kStep) {
     const int n0 = N - n12;
     if (n12 < max12) {
       head.clear();
