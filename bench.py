@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no timing output")
+    ap.add_argument("--oracle-gflop", type=float, default=0.0,
+                    help="oracle sample size in GFLOP (default: 150 per reference-arm step, 1000 for cpu_baseline)")
     return ap.parse_args()
 
 
@@ -178,12 +180,13 @@ def run_reference(args, rank, world):
     cfg = CONFIGS[args.config]
     # each step a smaller bounded sample (~0.15 TFLOP, a few seconds) so that the whole
     # --steps K --warmup W run ends within a few minutes
+    target = args.oracle_gflop * 1e9 if args.oracle_gflop > 0 else 0.15e12
     for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, 0.15e12)
+        cpu_oracle_sample(cfg, target)
     vals = []
     t_all = 0.0
     for _ in range(args.steps):
-        v, dt, desc, threads = cpu_oracle_sample(cfg, 0.15e12)
+        v, dt, desc, threads = cpu_oracle_sample(cfg, target)
         vals.append(v)
         t_all += dt
     value = statistics.median(vals)
@@ -476,7 +479,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, desc, threads = cpu_oracle_sample(cfg)
+        v, dt, desc, threads = cpu_oracle_sample(cfg, args.oracle_gflop * 1e9 if args.oracle_gflop > 0 else 1.0e12)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": desc,
                "seconds": dt}
 

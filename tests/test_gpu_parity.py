@@ -34,6 +34,7 @@ FP32_CASES = [
     dict(hq=2, hkv=1, seq=64, d=16, c=16),        # BASELINE configs[0] (tiny)
     dict(hq=4, hkv=1, seq=1024, d=64, c=256),     # one head group at 1K
     dict(hq=6, hkv=2, seq=96, d=20, c=32),        # odd G, odd d
+    dict(hq=2, hkv=1, seq=48, d=16, c=48),        # k = 1
 ]
 
 
@@ -75,6 +76,7 @@ BF16_CASES = [
     dict(hq=3, hkv=1, seq=768, d=64, c=384),      # d = 64, NH=1
     dict(hq=16, hkv=2, seq=640, d=128, c=128),    # G = 8, 5 chunks of the minimum size
     dict(hq=6, hkv=3, seq=1536, d=128, c=768),    # odd kv-head count, 6 query tiles per chunk
+    dict(hq=4, hkv=1, seq=384, d=128, c=384),     # k = 1: one chunk, SeCO = plain full attention
 ]
 
 
