@@ -78,11 +78,6 @@ constexpr int kWG = 4;          // compute warpgroups; WG w owns query columns {
 // reds clog the MIO queue that the mbarrier traffic of every role also uses.)
 
 constexpr int R0 = 0, R1 = 128, TM_DK = 256, TM_DV = 384;
-#ifndef SECO_BWD_EMU
-#define SECO_BWD_EMU 0
-#endif
-constexpr int kEmuPairs = SECO_BWD_EMU;
-   // of every 16 column pairs, this many use ex2_emu2 (FMA pipe)
 
 struct Args {
   int c, j, G, hkv, S;
@@ -101,7 +96,9 @@ struct Args {
   int* err;           // set to 1 if the dynamic smem window is not 1024-B aligned
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters] clock64
 };
+#ifdef SECO_TRACE
 constexpr int kTraceCtas = 4, kTraceSlots = 20, kTraceIters = 128;
+#endif
 }  // namespace bwd
 
 __global__ void __launch_bounds__(bwd::kThreads, 1)

@@ -68,7 +68,9 @@ struct Args {
   float* part_lse;            // nsplit > 1: [nsplit][hq][c] partial LSE (natural log)
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters]
 };
+#ifdef SECO_TRACE
 constexpr int kTraceCtas = 2, kTraceSlots = 24, kTraceIters = 256;
+#endif
 }  // namespace fwd
 
 template <int NH, int D, int STAGES>
