@@ -493,6 +493,405 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ============================================================================ backward v2
+// Same work decomposition, TMEM regions and MMAs as seco_bwd_sm100_kernel, with the issue order
+// of the CUTLASS / FlashAttention-4 Blackwell backward: per query tile i the MMA warp issues
+//   S^T(i+1) -> R0,  dK(i) += dS^T(i) Q(i),  dQ^T(i) -> R1,  dP^T(i+1) -> R1,  dV(i+1) += P^T(i+1) dO(i+1)
+// so the exponentials of tile i+1 (P^T, phase A) run while dK(i) / dQ^T(i) execute, and only
+// dQ^T drain -> dP^T(i+1) -> dS^T(i+1) (phase B) -> dK(i+1) -> dQ^T(i+1) stays serial.  dQ^T
+// lives in R1 (the dP^T region: dP^T(i) is dead once dS^T(i) is formed) and is drained by a
+// dedicated warpgroup into a two-slot 16 KiB staging ring (32 query rows x 128 d fp32 each),
+// from which one thread issues 1-D bulk reduce-adds; dO is single-buffered to make room.
+// Warps: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w3 dQ reduce issuer, w4-w7 dQ^T
+// drain (lane = d), w8-w15 two compute warpgroups (thread = key row, WG c owns query columns
+// [64c, 64c+64)).  Non-deterministic mode only (the deterministic mode keeps the v1 kernel).
+namespace bwd2 {
+constexpr int BKV = 128, BQ = 128, D = 128;
+constexpr int kTile = 128 * 128 * 2;           // bf16 [128][128]
+constexpr int kBox = 128 * 128;                // one [128 rows][128 B] box
+constexpr int kK = 0;
+constexpr int kV = kK + kTile;
+constexpr int kQ = kV + kTile;                 // two stages
+constexpr int kDO = kQ + 2 * kTile;            // one stage
+constexpr int kSTG = kDO + kTile;              // dQ staging: 2 slots x 16 KiB (contiguous after dO)
+constexpr int kSlot = 32 * D * 4;
+constexpr int kDS = kSTG + 2 * kSlot;          // dS^T [128 keys][128 q] bf16 (2 boxes by q half)
+constexpr int kStats = kDS + kTile;            // [2 stages][2][BQ] fp32 (-LSE log2e, D)
+constexpr int kBar = kStats + 2 * 2 * BQ * 4;
+constexpr int kNumBars = 20;
+constexpr int kTmemSlot = kBar + 8 * kNumBars;
+constexpr int kBytes = kTmemSlot + 16;
+constexpr int kThreads = 512;
+constexpr int R0 = 0, R1 = 128, TM_DK = 256, TM_DV = 384;
+}  // namespace bwd2
+
+__global__ void __launch_bounds__(bwd2::kThreads, 1)
+    seco_bwd2_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                           const __grid_constant__ CUtensorMap tm_dkv, const bwd::Args a) {
+  using namespace bwd2;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = smem_u32(smem);
+  if (sb & 1023) {
+    if (threadIdx.x == 0 && a.err) atomicExch(a.err, 1);
+    return;
+  }
+  const uint32_t sK = sb + kK, sV = sb + kV, sDO = sb + kDO, sDS = sb + kDS, sSTG = sb + kSTG;
+  auto qbuf = [&](int st) { return sb + kQ + (uint32_t)st * kTile; };
+  const uint32_t sStats = sb + kStats;
+  const uint32_t b0 = sb + kBar;
+  const uint32_t bar_kv = b0;
+  auto bar_q_full = [&](int s) { return b0 + 8u * (1 + s); };
+  auto bar_q_empty = [&](int s) { return b0 + 8u * (3 + s); };
+  const uint32_t bar_do_full = b0 + 8u * 5, bar_do_empty = b0 + 8u * 6;
+  const uint32_t bar_s_full = b0 + 8u * 7, bar_p_ready = b0 + 8u * 8;
+  const uint32_t bar_dp_full = b0 + 8u * 9, bar_ds_ready = b0 + 8u * 10;
+  const uint32_t bar_dq_full = b0 + 8u * 11, bar_dq_empty = b0 + 8u * 12;
+  auto bar_stg_full = [&](int s) { return b0 + 8u * (13 + s); };
+  auto bar_stg_free = [&](int s) { return b0 + 8u * (15 + s); };
+  const uint32_t bar_acc = b0 + 8u * 17, bar_drain_done = b0 + 8u * 18;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTmemSlot);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  // work decode: identical to seco_bwd_sm100_kernel (balanced list of units / query-range pieces)
+  const int bid = blockIdx.x;
+  int U, piece, f;
+  if (bid < a.n0) {
+    U = bid; piece = 0; f = 1;
+  } else if (bid < a.n0 + a.n1 * a.f1) {
+    const int r = bid - a.n0;
+    U = a.n0 + r / a.f1; piece = r % a.f1; f = a.f1;
+  } else {
+    const int r = bid - a.n0 - a.n1 * a.f1;
+    U = a.n0 + a.n1 + r / a.f2; piece = r % a.f2; f = a.f2;
+  }
+  const int g = U % a.hkv;
+  const int u = U / a.hkv;
+  const int k0 = u * BKV;
+  const int nqt = a.c / BQ;
+  const int rel = k0 - a.j * a.c;
+  const int qt_min = rel > 0 ? rel / BQ : 0;
+  const int n_all = a.G * (nqt - qt_min);
+  const int it0 = (int)((int64_t)piece * n_all / f);
+  const int it1 = (int)((int64_t)(piece + 1) * n_all / f);
+  const int n = it1 - it0;
+  struct Walk {
+    int hh, qt, G;
+    __device__ void next() { if (++hh == G) { hh = 0; ++qt; } }
+  };
+  const Walk walk0{it0 % a.G, qt_min + it0 / a.G, a.G};
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_kv, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar_q_full(s), 1);
+      mbar_init(bar_q_empty(s), 1);
+      mbar_init(bar_stg_full(s), 4);    // the 4 drain warps
+      mbar_init(bar_stg_free(s), 1);
+    }
+    mbar_init(bar_do_full, 1);
+    mbar_init(bar_do_empty, 1);
+    mbar_init(bar_s_full, 1);
+    mbar_init(bar_p_ready, 8);          // the 8 compute warps
+    mbar_init(bar_dp_full, 1);
+    mbar_init(bar_ds_ready, 8);
+    mbar_init(bar_dq_full, 1);
+    mbar_init(bar_dq_empty, 4);         // the 4 drain warps
+    mbar_init(bar_acc, 1);
+    mbar_init(bar_drain_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_q); tma_prefetch(&tm_do); tma_prefetch(&tm_k); tma_prefetch(&tm_v);
+    tma_prefetch(&tm_dkv);
+  }
+  if (warp == 2) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (n > 0) {
+    if (warp == 0) {
+      // -------------------------------------------------------------- TMA producer
+      if (lane == 0) {
+        mbar_expect_tx(bar_kv, 2 * kTile);
+        for (int x = 0; x < D / 64; ++x) {
+          tma_load_3d(sK + x * kBox, &tm_k, bar_kv, x * 64, k0, g);
+          tma_load_3d(sV + x * kBox, &tm_v, bar_kv, x * 64, k0, g);
+        }
+        Walk w = walk0;
+        for (int i = 0; i < n; ++i, w.next()) {
+          const int st = i & 1;
+          const uint32_t ph = (i >> 1) & 1;
+          const int h = g * a.G + w.hh, qt = w.qt;
+          mbar_wait(bar_q_empty(st), ph ^ 1);
+          mbar_expect_tx(bar_q_full(st), kTile + 2 * BQ * 4);
+          for (int x = 0; x < D / 64; ++x)
+            tma_load_3d(qbuf(st) + x * kBox, &tm_q, bar_q_full(st), x * 64, qt * BQ, h);
+          const int64_t ro = (int64_t)h * a.c + qt * BQ;
+          bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_q_full(st));
+          bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_q_full(st));
+          mbar_wait(bar_do_empty, (i & 1) ^ 1);
+          mbar_expect_tx(bar_do_full, kTile);
+          for (int x = 0; x < D / 64; ++x)
+            tma_load_3d(sDO + x * kBox, &tm_do, bar_do_full, x * 64, qt * BQ, h);
+        }
+      }
+    } else if (warp == 1) {
+      // -------------------------------------------------------------- MMA issuer
+      if (lane == 0) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(BKV, BQ, 0, 0);
+        constexpr uint32_t idesc_kv = make_idesc_bf16(BKV, D, 0, 1);
+        constexpr uint32_t idesc_q = make_idesc_bf16(D, BQ, 1, 1);
+        auto issue_sdp = [&](uint32_t a_base, uint32_t b_base, uint32_t d_col) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * kBox + (kk % 4) * 32;
+            mma_ss(tmem + d_col, make_desc_sw128(a_base + off, 16, 1024), make_desc_sw128(b_base + off, 16, 1024),
+                   idesc_s, kk > 0);
+          }
+        };
+        // A = P^T / dS^T packed in TMEM (query k-step kk at columns base + 16 kk .. +7)
+        auto issue_kv = [&](uint32_t a_col, uint32_t b_base, uint32_t d_col, bool acc) {
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            mma_ts(tmem + d_col, tmem + a_col + 16 * kk, make_desc_sw128(b_base + kk * 2048, kBox, 1024), idesc_kv,
+                   (acc || kk > 0) ? 1u : 0u);
+        };
+        mbar_wait(bar_kv, 0);
+        mbar_wait(bar_q_full(0), 0);
+        tc_fence_after();
+        issue_sdp(sK, qbuf(0), R0);                       // S^T(0)
+        mma_commit(bar_s_full);
+        mbar_wait(bar_do_full, 0);
+        tc_fence_after();
+        issue_sdp(sV, sDO, R1);                           // dP^T(0)
+        mma_commit(bar_dp_full);
+        mbar_wait(bar_p_ready, 0);
+        tc_fence_after();
+        issue_kv(R0, sDO, TM_DV, false);                  // dV = P^T(0) dO(0)
+        mma_commit(bar_do_empty);
+        for (int i = 0; i < n; ++i) {
+          const int st = i & 1;
+          const bool more = i + 1 < n;
+          if (more) {                                     // S^T(i+1) -> R0 (P^T(i) consumed by dV(i))
+            mbar_wait(bar_q_full(st ^ 1), ((i + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_sdp(sK, qbuf(st ^ 1), R0);
+            mma_commit(bar_s_full);
+          }
+          mbar_wait(bar_ds_ready, i & 1);                 // dK(i) += dS^T(i) Q(i)
+          tc_fence_after();
+          issue_kv(R1, qbuf(st), TM_DK, i > 0);
+          mma_commit(bar_q_empty(st));
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)           // dQ^T(i) = K^T dS^T(i) -> R1
+            mma_ss(tmem + R1, make_desc_sw128(sK + kk * 2048, kBox, 1024),
+                   make_desc_sw128(sDS + kk * 2048, kBox, 1024), idesc_q, kk > 0);
+          mma_commit(bar_dq_full);
+          if (more) {
+            mbar_wait(bar_dq_empty, i & 1);               // dQ^T(i) drained from R1
+            mbar_wait(bar_do_full, (i + 1) & 1);
+            tc_fence_after();
+            issue_sdp(sV, sDO, R1);                       // dP^T(i+1)
+            mma_commit(bar_dp_full);
+            mbar_wait(bar_p_ready, (i + 1) & 1);
+            tc_fence_after();
+            issue_kv(R0, sDO, TM_DV, true);               // dV += P^T(i+1) dO(i+1)
+            mma_commit(bar_do_empty);
+          }
+        }
+        mma_commit(bar_acc);
+      }
+    } else if (warp == 3) {
+      // -------------------------------------------------------------- dQ reduce issuer
+      if (lane == 0) {
+        Walk w = walk0;
+        int m = 0;                                        // staged chunk sequence number
+        for (int i = 0; i < n; ++i, w.next()) {
+          const int h = g * a.G + w.hh, qt = w.qt;
+          float* dst = a.dqacc + ((int64_t)h * a.c + qt * BQ) * D;
+          for (int c = 0; c < 4; ++c, ++m) {
+            const int s = c & 1;
+            mbar_wait(bar_stg_full(s), (m >> 1) & 1);
+            bulk_reduce_add_f32(dst + 32 * c * D, sSTG + s * kSlot, kSlot);
+            bulk_commit();
+            if (m > 0) {
+              bulk_wait_read<1>();                        // the previous chunk's slot was read
+              mbar_arrive(bar_stg_free(s ^ 1));
+            }
+          }
+        }
+        bulk_wait_read<0>();
+        mbar_arrive(bar_stg_free((m - 1) & 1));
+        bulk_wait0();
+        mbar_arrive(bar_drain_done);
+      }
+    } else if (warp >= 4 && warp < 8) {
+      // -------------------------------------------------------------- dQ^T drain (lane = d)
+      const int wq = warp % 4;
+      const int dr = wq * 32 + lane;
+      const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+      int m = 0;
+      auto stage = [&](const uint32_t (&v)[32], int s) {
+        mbar_wait(bar_stg_free(s), ((m >> 1) & 1) ^ 1);
+        const uint32_t base = sSTG + s * kSlot + dr * 4;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) st_shared_f32(base + q * (D * 4), __uint_as_float(v[q]));
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_stg_full(s));
+        ++m;
+      };
+      for (int i = 0; i < n; ++i) {
+        mbar_wait(bar_dq_full, i & 1);
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld32(tmem + lane_addr + R1, v0);
+        tmem_wait_ld();
+        stage(v0, 0);
+        tmem_ld32(tmem + lane_addr + R1 + 32, v1);
+        tmem_wait_ld();
+        stage(v1, 1);
+        tmem_ld32(tmem + lane_addr + R1 + 64, v0);
+        tmem_ld32(tmem + lane_addr + R1 + 96, v1);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_dq_empty);        // R1 free for dP^T(i+1)
+        stage(v0, 0);
+        stage(v1, 1);
+      }
+    } else if (warp >= 8) {
+      // -------------------------------------------------------------- compute warpgroups
+      const int cw = (warp - 8) / 4;                      // query columns [64 cw, 64 cw + 64)
+      const int wq = warp % 4;
+      const int kr = wq * 32 + lane;                      // key row within the tile
+      const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+      const int key_pos = k0 + kr;
+      const f2_t sl2x2 = f2(a.scale_log2, a.scale_log2);
+      Walk w = walk0;
+      for (int i = 0; i < n; ++i, w.next()) {
+        const int st = i & 1;
+        const int qbase = a.j * a.c + w.qt * BQ;
+        float p[64];
+        // ---- phase A: P^T = exp2(S^T sigma log2e - LSE log2e) -> bf16 over R0
+        mbar_wait(bar_q_full(st), (i >> 1) & 1);
+        mbar_wait(bar_s_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          const int c = 64 * cw + 32 * sub;
+          uint32_t sv[32];
+          tmem_ld32(tmem + lane_addr + R0 + c, sv);
+          tmem_wait_ld();
+          const uint32_t nl_s = sStats + (st * 2 * BQ + c) * 4;
+          const int qpos0 = qbase + c;
+          const bool masked = (k0 + wq * 32 + 31) > qpos0;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 L = ld_shared_f4(nl_s + c4 * 16);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int c2 = c4 * 4 + h2 * 2;
+              const f2_t x = ffma2(f2u(sv[c2], sv[c2 + 1]), sl2x2, h2 ? f2(L.z, L.w) : f2(L.x, L.y));
+              float p0 = ex2(f2lo(x)), p1 = ex2(f2hi(x));
+              if (masked) {
+                if (key_pos > qpos0 + c2) p0 = 0.f;
+                if (key_pos > qpos0 + c2 + 1) p1 = 0.f;
+              }
+              p[32 * sub + c2] = p0;
+              p[32 * sub + c2 + 1] = p1;
+            }
+          }
+#pragma unroll
+          for (int k2 = 0; k2 < 2; ++k2) {               // query k-steps c/16 + k2 -> columns 16 kk .. +7
+            uint32_t pp[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pp[q] = pack_bf16(p[32 * sub + 16 * k2 + 2 * q], p[32 * sub + 16 * k2 + 2 * q + 1]);
+            tmem_st8(tmem + lane_addr + R0 + c + 16 * k2, pp);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_p_ready);
+        // ---- phase B: dS^T = P^T o (dP^T - D) -> bf16 over R1 and to smem (dQ^T operand)
+        mbar_wait(bar_dp_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          const int c = 64 * cw + 32 * sub;
+          uint32_t dpv[32];
+          tmem_ld32(tmem + lane_addr + R1 + c, dpv);
+          tmem_wait_ld();
+          const uint32_t d_s = sStats + (st * 2 * BQ + BQ + c) * 4;
+          uint32_t dd[16];
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 Dv = ld_shared_f4(d_s + c4 * 16);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int c2 = c4 * 4 + h2 * 2;
+              const f2_t ds2 = fmul2(f2(p[32 * sub + c2], p[32 * sub + c2 + 1]),
+                                     fsub2(f2u(dpv[c2], dpv[c2 + 1]), h2 ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y)));
+              dd[c2 / 2] = pack_bf16_f2(ds2);
+            }
+          }
+          tmem_st8(tmem + lane_addr + R1 + c, *reinterpret_cast<const uint32_t(*)[8]>(dd));
+          tmem_st8(tmem + lane_addr + R1 + c + 16, *reinterpret_cast<const uint32_t(*)[8]>(dd + 8));
+          // dS^T to smem: box c / 64 (query half), row kr, 16-B chunks (c % 64) / 8 .. +3
+          const uint32_t drow = sDS + (c / 64) * kBox;
+          const int ch = (c % 64) / 8;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(drow + sw128_off(kr, ch + q), dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]);
+        }
+        tmem_wait_st();
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_ds_ready);
+      }
+      // ---- epilogue: WG 0 -> dK, WG 1 -> dV: TMEM -> scaled fp32 swizzled boxes -> TMA reduce-add
+      mbar_wait(bar_acc, 0);
+      mbar_wait(bar_drain_done, 0);
+      tc_fence_after();
+      const int mat = cw;
+      const float sc = mat == 0 ? a.dk_scale : a.dv_scale;
+      auto stg_box = [&](int cc) { return (mat == 0 ? sb + kQ : sDO) + (uint32_t)cc * kBox; };
+#pragma unroll 1
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_addr + (mat == 0 ? TM_DK : TM_DV) + cc * 32, v);
+        tmem_wait_ld();
+        const uint32_t box = stg_box(cc);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          st_shared_v4(box + sw128_off(kr, q), __float_as_uint(sc * __uint_as_float(v[4 * q])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 1])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 2])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 3])));
+      }
+      fence_async_smem();
+      named_bar_sync(2 + mat, 128);
+      if (wq == 0 && lane == 0) {
+        const int row0 = (mat * a.hkv + g) * a.S + k0;
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
+        bulk_commit();
+        bulk_wait0();
+      }
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 namespace {
 // ---- work list for one backward call (host side) ------------------------------------------
 // Units (key tile u of kv-head g) cost G * (query tiles that see the tile) 128x128 blocks: the
@@ -621,15 +1020,22 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              const CUtensorMap& tdkv, const void* o, const void* d_o,
                              const float* lse, float relay, float gscale, float* dkv, void* dq, void* dk_own,
                              void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st, int* launches) {
-  static_assert(bwd::kBytes <= 232448, "shared memory budget");
+  static_assert(bwd::kBytes <= 232448 && bwd2::kBytes <= 232448, "shared memory budget");
   // d = 64 runs on zero-padded 128-column tiles (TMA out-of-bounds fill on load; the dK/dV
   // reduce-add boxes past column 64 are dropped by the same bounds check; dQacc rows are 128)
   if ((g.d != bwd::D && g.d != 64) || g.c % bwd::BQ) return cudaErrorInvalidValue;
   int* order = g.det ? reinterpret_cast<int*>(ws_D + 2 * (size_t)g.hq * g.c) : nullptr;
   cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.c, relay, st, order);
   if (e != cudaSuccess) return e;
-  static std::atomic<unsigned long long> attr_done{0};
-  if ((e = ensure_smem_attr(seco_bwd_sm100_kernel, bwd::kBytes, attr_done)) != cudaSuccess) return e;
+  static std::atomic<unsigned long long> attr_done{0}, attr_done2{0};
+  static const bool v2 = [] {
+    const char* e2 = std::getenv("SECO_BWD_V2");   // experiment switch (A/B of the two backwards)
+    return e2 != nullptr && e2[0] == '1';
+  }();
+  const bool use_v2 = v2 && !g.det;
+  if ((e = use_v2 ? ensure_smem_attr(seco_bwd2_sm100_kernel, bwd2::kBytes, attr_done2)
+                  : ensure_smem_attr(seco_bwd_sm100_kernel, bwd::kBytes, attr_done)) != cudaSuccess)
+    return e;
   bwd::Args a;
   a.c = g.c; a.j = g.j; a.G = g.hq / g.hkv; a.hkv = g.hkv; a.S = g.c * g.k;
   a.scale_log2 = g.scale * 1.4426950408889634f;
@@ -653,7 +1059,10 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                            : choose_schedule(g.c, g.j, g.hkv, a.G, num_sms());
   a.n0 = sc.n0; a.n1 = sc.n1; a.f1 = sc.f1; a.f2 = sc.f2;
   dim3 grid(sc.grid);
-  seco_bwd_sm100_kernel<<<grid, bwd::kThreads, bwd::kBytes, st>>>(tq, tdo, tk, tv, tdq, tdkv, a);
+  if (use_v2)
+    seco_bwd2_sm100_kernel<<<grid, bwd2::kThreads, bwd2::kBytes, st>>>(tq, tdo, tk, tv, tdkv, a);
+  else
+    seco_bwd_sm100_kernel<<<grid, bwd::kThreads, bwd::kBytes, st>>>(tq, tdo, tk, tv, tdq, tdkv, a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   e = launch_final_bf16(g, ws_dqacc, dq, dkv, dk_own, dv_own, gscale * g.scale, st);
   *launches = 2 + 1;
