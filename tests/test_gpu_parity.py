@@ -247,3 +247,35 @@ def test_bf16_chunked_attention_sequence_major_layout():
     assert err(host(layer.dkv[1]), ref["dv"]) <= BF16_TOL
     with pytest.raises(ValueError):
         layer.seco_step(*upload(x, torch.bfloat16))          # head-major inputs: wrong strides
+
+
+def test_bf16_backward_v2_issue_order_subprocess():
+    """The experimental backward (SECO_BWD_V2=1: CUTLASS / FA4 issue order, dQ^T drained from the
+    dP^T region through a staging ring) matches the oracle too.  The switch is read
+    once per process, so the check runs in a child process."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import chunkwise as OC
+from tests.gpu_util import BF16_TOL, err, host, inputs, upload
+from paper_2505_16710_b200.step import ChunkedAttention
+for (hq, hkv, seq, c) in ((8, 2, 512, 128), (4, 1, 1024, 256), (3, 1, 768, 384)):
+    x = inputs(hq, hkv, seq, 128, seed=5, peaky=True)
+    q, k, v, do = upload(x, torch.bfloat16)
+    L = ChunkedAttention(hq, hkv, 128, seq, c, dtype=torch.bfloat16)
+    L.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    ref = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (seq // c))
+    dk, dv = L.own_grads()
+    for name, gpu in (("dq", host(L.dq)), ("dk", host(dk)), ("dv", host(dv))):
+        e = err(gpu, ref[name])
+        assert e <= BF16_TOL, (hq, hkv, seq, c, name, e)
+print("v2 ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, SECO_BWD_V2="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "v2 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
