@@ -552,6 +552,15 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
   const uint32_t bar_acc = b0 + 8u * 17, bar_drain_done = b0 + 8u * 18;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTmemSlot);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#ifdef SECO_TRACE
+#define V2TRACE(slot, i)                                                                                   \
+  do {                                                                                                     \
+    if (a.trace && blockIdx.x < bwd::kTraceCtas && (i) < bwd::kTraceIters)                                \
+      a.trace[((size_t)blockIdx.x * bwd::kTraceSlots + (slot)) * bwd::kTraceIters + (i)] = clock64();     \
+  } while (0)
+#else
+#define V2TRACE(slot, i) do { } while (0)
+#endif
 
   // work decode: identical to seco_bwd_sm100_kernel (balanced list of units / query-range pieces)
   const int bid = blockIdx.x;
@@ -632,10 +641,12 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
           const int64_t ro = (int64_t)h * a.c + qt * BQ;
           bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_q_full(st));
           bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_q_full(st));
+          V2TRACE(0, i);
           mbar_wait(bar_do_empty, (i & 1) ^ 1);
           mbar_expect_tx(bar_do_full, kTile);
           for (int x = 0; x < D / 64; ++x)
             tma_load_3d(sDO + x * kBox, &tm_do, bar_do_full, x * 64, qt * BQ, h);
+          V2TRACE(1, i);
         }
       }
     } else if (warp == 1) {
@@ -680,23 +691,32 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
             tc_fence_after();
             issue_sdp(sK, qbuf(st ^ 1), R0);
             mma_commit(bar_s_full);
+            V2TRACE(2, i);
           }
-          mbar_wait(bar_ds_ready, i & 1);                 // dK(i) += dS^T(i) Q(i)
+          mbar_wait(bar_ds_ready, i & 1);
+          V2TRACE(3, i);
           tc_fence_after();
-          issue_kv(R1, qbuf(st), TM_DK, i > 0);
-          mma_commit(bar_q_empty(st));
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)           // dQ^T(i) = K^T dS^T(i) -> R1
-            mma_ss(tmem + R1, make_desc_sw128(sK + kk * 2048, kBox, 1024),
+          for (int kk = 0; kk < BKV / 16; ++kk)           // dQ^T(i) = K^T dS^T(i) -> R1 (first: it
+            mma_ss(tmem + R1, make_desc_sw128(sK + kk * 2048, kBox, 1024),   // heads the serial chain)
                    make_desc_sw128(sDS + kk * 2048, kBox, 1024), idesc_q, kk > 0);
           mma_commit(bar_dq_full);
+          V2TRACE(4, i);
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk)            // dK(i) += dS^T(i) Q(i), A = dS^T from smem
+            mma_ss(tmem + TM_DK, make_desc_sw128(sDS + (kk / 4) * kBox + (kk % 4) * 32, 16, 1024),
+                   make_desc_sw128(qbuf(st) + kk * 2048, kBox, 1024), idesc_kv, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(bar_q_empty(st));
           if (more) {
             mbar_wait(bar_dq_empty, i & 1);               // dQ^T(i) drained from R1
+            V2TRACE(5, i);
             mbar_wait(bar_do_full, (i + 1) & 1);
+            V2TRACE(6, i);
             tc_fence_after();
             issue_sdp(sV, sDO, R1);                       // dP^T(i+1)
             mma_commit(bar_dp_full);
             mbar_wait(bar_p_ready, (i + 1) & 1);
+            V2TRACE(7, i);
             tc_fence_after();
             issue_kv(R0, sDO, TM_DV, true);               // dV += P^T(i+1) dO(i+1)
             mma_commit(bar_do_empty);
@@ -717,6 +737,8 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
             mbar_wait(bar_stg_full(s), (m >> 1) & 1);
             bulk_reduce_add_f32(dst + 32 * c * D, sSTG + s * kSlot, kSlot);
             bulk_commit();
+            if (c == 0) V2TRACE(16, i);
+            if (c == 3) V2TRACE(17, i);
             if (m > 0) {
               bulk_wait_read<1>();                        // the previous chunk's slot was read
               mbar_arrive(bar_stg_free(s ^ 1));
@@ -746,6 +768,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
       };
       for (int i = 0; i < n; ++i) {
         mbar_wait(bar_dq_full, i & 1);
+        if (lane == 0 && wq == 0) V2TRACE(13, i);
         tc_fence_after();
         uint32_t v0[32], v1[32];
         tmem_ld32(tmem + lane_addr + R1, v0);
@@ -760,8 +783,10 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_dq_empty);        // R1 free for dP^T(i+1)
+        if (lane == 0 && wq == 0) V2TRACE(14, i);
         stage(v0, 0);
         stage(v1, 1);
+        if (lane == 0 && wq == 0) V2TRACE(15, i);
       }
     } else if (warp >= 8) {
       // -------------------------------------------------------------- compute warpgroups
@@ -775,15 +800,17 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
       for (int i = 0; i < n; ++i, w.next()) {
         const int st = i & 1;
         const int qbase = a.j * a.c + w.qt * BQ;
-        float p[64];
+        uint32_t pk[32];                                  // P^T of this thread's 64 queries, bf16 pairs
         // ---- phase A: P^T = exp2(S^T sigma log2e - LSE log2e) -> bf16 over R0
         mbar_wait(bar_q_full(st), (i >> 1) & 1);
         mbar_wait(bar_s_full, i & 1);
+        if (lane == 0 && wq == 0 && cw == 0) V2TRACE(8, i);
         tc_fence_after();
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {
           const int c = 64 * cw + 32 * sub;
           uint32_t sv[32];
+          float p[32];
           tmem_ld32(tmem + lane_addr + R0 + c, sv);
           tmem_wait_ld();
           const uint32_t nl_s = sStats + (st * 2 * BQ + c) * 4;
@@ -801,15 +828,18 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
                 if (key_pos > qpos0 + c2) p0 = 0.f;
                 if (key_pos > qpos0 + c2 + 1) p1 = 0.f;
               }
-              p[32 * sub + c2] = p0;
-              p[32 * sub + c2 + 1] = p1;
+              p[c2] = p0;
+              p[c2 + 1] = p1;
             }
           }
 #pragma unroll
           for (int k2 = 0; k2 < 2; ++k2) {               // query k-steps c/16 + k2 -> columns 16 kk .. +7
             uint32_t pp[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) pp[q] = pack_bf16(p[32 * sub + 16 * k2 + 2 * q], p[32 * sub + 16 * k2 + 2 * q + 1]);
+            for (int q = 0; q < 8; ++q) {
+              pp[q] = pack_bf16(p[16 * k2 + 2 * q], p[16 * k2 + 2 * q + 1]);
+              pk[16 * sub + 8 * k2 + q] = pp[q];
+            }
             tmem_st8(tmem + lane_addr + R0 + c + 16 * k2, pp);
           }
         }
@@ -817,15 +847,19 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p_ready);
-        // ---- phase B: dS^T = P^T o (dP^T - D) -> bf16 over R1 and to smem (dQ^T operand)
+        if (lane == 0 && wq == 0 && cw == 0) V2TRACE(9, i);
+        // ---- phase B: dS^T = P^T o (dP^T - D) (P^T as rounded for the dV MMA) -> bf16 to smem,
+        // the A operand of dK and the B operand of dQ^T
         mbar_wait(bar_dp_full, i & 1);
+        if (lane == 0 && wq == 0 && cw == 0) V2TRACE(10, i);
         tc_fence_after();
+        uint32_t dpv[64];
+        tmem_ld32(tmem + lane_addr + R1 + 64 * cw, *reinterpret_cast<uint32_t(*)[32]>(dpv));
+        tmem_ld32(tmem + lane_addr + R1 + 64 * cw + 32, *reinterpret_cast<uint32_t(*)[32]>(dpv + 32));
+        tmem_wait_ld();
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {
           const int c = 64 * cw + 32 * sub;
-          uint32_t dpv[32];
-          tmem_ld32(tmem + lane_addr + R1 + c, dpv);
-          tmem_wait_ld();
           const uint32_t d_s = sStats + (st * 2 * BQ + BQ + c) * 4;
           uint32_t dd[16];
 #pragma unroll
@@ -834,13 +868,13 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
               const int c2 = c4 * 4 + h2 * 2;
-              const f2_t ds2 = fmul2(f2(p[32 * sub + c2], p[32 * sub + c2 + 1]),
-                                     fsub2(f2u(dpv[c2], dpv[c2 + 1]), h2 ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y)));
+              const uint32_t pw = pk[16 * sub + c2 / 2];
+              const f2_t p2 = f2(__uint_as_float(pw << 16), __uint_as_float(pw & 0xffff0000u));
+              const f2_t ds2 = fmul2(p2, fsub2(f2u(dpv[32 * sub + c2], dpv[32 * sub + c2 + 1]),
+                                               h2 ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y)));
               dd[c2 / 2] = pack_bf16_f2(ds2);
             }
           }
-          tmem_st8(tmem + lane_addr + R1 + c, *reinterpret_cast<const uint32_t(*)[8]>(dd));
-          tmem_st8(tmem + lane_addr + R1 + c + 16, *reinterpret_cast<const uint32_t(*)[8]>(dd + 8));
           // dS^T to smem: box c / 64 (query half), row kr, 16-B chunks (c % 64) / 8 .. +3
           const uint32_t drow = sDS + (c / 64) * kBox;
           const int ch = (c % 64) / 8;
@@ -853,6 +887,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_ds_ready);
+        if (lane == 0 && wq == 0) V2TRACE(cw == 0 ? 11 : 12, i);
       }
       // ---- epilogue: WG 0 -> dK, WG 1 -> dV: TMEM -> scaled fp32 swizzled boxes -> TMA reduce-add
       mbar_wait(bar_acc, 0);
@@ -1029,8 +1064,8 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   if (e != cudaSuccess) return e;
   static std::atomic<unsigned long long> attr_done{0}, attr_done2{0};
   static const bool v2 = [] {
-    const char* e2 = std::getenv("SECO_BWD_V2");   // experiment switch (A/B of the two backwards)
-    return e2 != nullptr && e2[0] == '1';
+    const char* e2 = std::getenv("SECO_BWD_V2");   // A/B switch: SECO_BWD_V2=0 selects the v1 kernel
+    return e2 == nullptr || e2[0] != '0';
   }();
   const bool use_v2 = v2 && !g.det;
   if ((e = use_v2 ? ensure_smem_attr(seco_bwd2_sm100_kernel, bwd2::kBytes, attr_done2)
