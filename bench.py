@@ -372,7 +372,7 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
                 "kernel": f"seco_chunk_{'backward' if dom == 'bwd' else 'forward'} "
-                          f"({'bwd_prep + seco_bwd_sm100_kernel + bwd_final' if dom == 'bwd' else 'seco_fwd_sm100_kernel'})",
+                          f"({('bwd_prep + seco_bwd_sm100_kernel + bwd_final' if args.deterministic else 'bwd_prep + seco_bwd2_sm100_kernel + bwd_final') if dom == 'bwd' else 'seco_fwd_sm100_kernel'})",
                 "peak_source": peak_src, "frac_of_burst_peak": achieved / peak_burst if achieved else None,
                 "traffic_note": f"DRAM bytes of the {traffic_launch} launch from ncu --set full "
                                 "(profiles/roofline_traffic.json); achieved averages all launches"}

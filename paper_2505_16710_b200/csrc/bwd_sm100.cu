@@ -30,6 +30,10 @@
 // s), through swizzled smem staging and TMA reduce-add into dkv; slot j of dkv was
 // pre-scaled by the relay factor gamma in bwd_prep (grad_hook).
 // All fp32 reductions are issued by the TMA unit: no per-element atomics.
+//
+// This header describes v1 (seco_bwd_sm100_kernel, the deterministic-mode kernel).  The default
+// kernel is v2 (seco_bwd2_sm100_kernel, further down): same regions and MMAs in the CUTLASS /
+// FlashAttention-4 issue order, see its own header and DESIGN §6.2.
 #include "common.cuh"
 #include "kernels.h"
 
