@@ -36,8 +36,10 @@
  * Ownership: the caller owns every buffer (device memory), including dkv, which
  * the caller zeroes once per training step.  The library never allocates device
  * memory, never synchronises, and enqueues all work on `stream`.  Host-side
- * state: a mutex-guarded cache of kernel attributes only.  All functions are
- * reentrant.
+ * state: mutex-guarded caches of kernel attributes, backward work lists and TMA
+ * tensor maps (keyed by pointer, sizes and strides; a tensor map holds no data, so
+ * a cached map of a freed and re-allocated buffer with the same key is still
+ * exact).  All functions are reentrant.
  *
  * Errors: return codes only, nothing throws across the ABI.  Arguments are
  * validated on the host before any launch (SECO_ERR_ARG: null pointer, j out of
@@ -84,6 +86,18 @@ typedef struct {
  * combine).  Costs backward throughput: the first wave of CTAs orders itself. */
 #define SECO_FLAG_DETERMINISTIC 1
 
+/* flags: SECO_FLAG_PREV_INDEPENDENT is the caller's promise, for seco_chunk_forward,
+ * that the kernel enqueued on `stream` immediately before the call writes none of the
+ * call's inputs (q, k_cache, v_cache) and reads none of its outputs (o, lse) -- e.g.
+ * the previous chunk's forward in stage 1 (Alg. 1 lines 1-3 P:195-197).  The forward
+ * may then load its inputs while that kernel's last wave drains (programmatic
+ * dependent launch).  Without the flag the forward still overlaps its prologue
+ * (barrier init, TMEM allocation) with the predecessor, but waits for the
+ * predecessor's completion and memory visibility before its first global load or
+ * store.  In both cases the forward completes only after its predecessor did, so
+ * work enqueued after it sees normal stream order.  Ignored by the other calls. */
+#define SECO_FLAG_PREV_INDEPENDENT 2
+
 /* Bytes of device workspace `ws` the two chunk calls need (dQ accumulator,
  * row statistics).  Same for every j. */
 size_t seco_workspace_size(const seco_shape* shape);
@@ -120,6 +134,20 @@ seco_status seco_chunk_backward(const seco_shape* shape, int32_t j,
                                 float relay_scale, float grad_scale,
                                 float* dkv, void* dq, void* dk_own, void* dv_own,
                                 void* ws, size_t ws_bytes, seco_stream_t stream);
+
+/* SpaCO, a chunk j that is NOT in the sampled set I (Alg. 2 line 5 "for i in I"
+ * skips it; reading Z11): its gradients are zero and its checkpoint gradient is
+ * never relayed.  Effects, enqueued on `stream`:
+ *   dq                    = 0   ([hq][c][d] chunk view, q strides of `shape`)
+ *   dkv[:, :, slot j]     = 0   (the deposits of later chunks into slot j are dropped)
+ *   dk_own, dv_own        = 0   (skipped if NULL)
+ * Call it at chunk j's place in the descending stage-2 walk, i.e. after every
+ * sampled chunk > j has run its backward (those are the only depositors into slot
+ * j).  After a SpaCO step dkv then holds exactly the per-chunk own gradients.
+ * Errors: as seco_chunk_backward (SECO_ERR_ARG for a NULL dq / dkv, bad shape, j out
+ * of range, misaligned pointer). */
+seco_status spaco_chunk_skip(const seco_shape* shape, int32_t j, float* dkv, void* dq, void* dk_own,
+                             void* dv_own, seco_stream_t stream);
 
 /* SpaCO sampling (Alg. 2 line 4 P:329 "Randomly select t distinct indices") and
  * scales (cap P:415), on the host, integer-only PRNG (splitmix64, state =

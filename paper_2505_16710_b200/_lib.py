@@ -13,7 +13,8 @@ SECO_OK, SECO_ERR_ARG, SECO_ERR_UNSUPPORTED, SECO_ERR_CUDA = 0, 1, 2, 3
 SECO_BF16, SECO_FP32_DEBUG = 0, 1
 SPACO_PAPER, SPACO_HT, SPACO_BERNOULLI = 0, 1, 2
 
-EXPORTS = ("seco_workspace_size", "seco_chunk_forward", "seco_chunk_backward", "spaco_sample_and_scale",
+EXPORTS = ("seco_workspace_size", "seco_chunk_forward", "seco_chunk_backward", "spaco_chunk_skip",
+           "spaco_sample_and_scale",
            "seco_lora_workspace_size", "seco_lora_grad",
            "seco_status_string", "seco_last_error", "seco_last_launch_count", "seco_debug_bwd_schedule")
 
@@ -28,6 +29,7 @@ class SecoShape(ctypes.Structure):
 
 
 SECO_FLAG_DETERMINISTIC = 1
+SECO_FLAG_PREV_INDEPENDENT = 2
 
 
 class LoraShape(ctypes.Structure):
@@ -60,6 +62,8 @@ def load():
     lib.seco_chunk_backward.argtypes = [P(SecoShape), i32, vp, vp, vp, vp, vp, vp, f32, f32,
                                         vp, vp, vp, vp, vp, sz, vp]
     lib.seco_chunk_backward.restype = i32
+    lib.spaco_chunk_skip.argtypes = [P(SecoShape), i32, vp, vp, vp, vp, vp]
+    lib.spaco_chunk_skip.restype = i32
     lib.spaco_sample_and_scale.argtypes = [i32, i32, ctypes.c_uint64, f32, i32, P(i32), P(i32), P(f32), P(f32)]
     lib.spaco_sample_and_scale.restype = i32
     lib.seco_lora_workspace_size.argtypes = [P(LoraShape)]

@@ -185,6 +185,65 @@ cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, 
                                      reinterpret_cast<__nv_bfloat16*>(dv_own), dq_scale, st);
 }
 
+// ===================================================================== SpaCO skipped chunk
+// Alg. 2 line 5 ("for i in I") never visits a chunk outside the sample: its dQ, own
+// dK / dV are zero and the deposits later chunks made into its checkpoint slot are dropped
+// (reading Z11).  Blocks [0, nQ): dq rows (strided, element type T) = 0; the rest: dkv slot j
+// (both tensors, every kv head, fp32) = 0 and the optional own copies = 0.  16-B stores
+// (d % 4 == 0 on every path, so a dkv slot and a dense own copy are 16-B aligned whenever
+// their base pointers are -- checked by the ABI).
+struct SkipArgs {
+  int hq, hkv, c, d, j, S;
+  int64_t qh, qr;
+  int nQ, nK;
+};
+template <typename T>
+__global__ void __launch_bounds__(256) chunk_skip_kernel(float* __restrict__ dkv, T* __restrict__ dq,
+                                                         T* __restrict__ dk_own, T* __restrict__ dv_own,
+                                                         SkipArgs a) {
+  const int bid = blockIdx.x;
+  const int dv4 = a.d / 4;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (bid < a.nQ) {
+    const int64_t total = (int64_t)a.hq * a.c * dv4;
+    for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < total; i += (int64_t)a.nQ * blockDim.x) {
+      const int64_t row = i / dv4;
+      const int x = (int)(i - row * dv4) * 4;
+      const int64_t h = row / a.c, r = row - h * a.c;
+      T* dst = dq + h * a.qh + r * a.qr + x;   // element stores: dq strides need no 16-B alignment
+#pragma unroll
+      for (int e = 0; e < 4; ++e) stf(dst + e, 0.f);
+    }
+  } else {
+    const int64_t per4 = (int64_t)a.c * dv4;
+    const int64_t total = 2 * (int64_t)a.hkv * per4;
+    for (int64_t i = (int64_t)(bid - a.nQ) * blockDim.x + threadIdx.x; i < total; i += (int64_t)a.nK * blockDim.x) {
+      const int64_t th = i / per4, off4 = i - th * per4;
+      reinterpret_cast<float4*>(dkv + th * (int64_t)a.S * a.d + (int64_t)a.j * a.c * a.d)[off4] = z;
+      T* own = th < a.hkv ? dk_own : dv_own;
+      if (own) Vec4<T>::store(own + (th % a.hkv) * per4 * 4 + off4 * 4, z);
+    }
+  }
+}
+
+cudaError_t launch_chunk_skip(const ChunkGeom& g, bool bf16, float* dkv, void* dq, void* dk_own, void* dv_own,
+                              cudaStream_t st) {
+  SkipArgs a;
+  a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
+  a.qh = g.qh; a.qr = g.qr;
+  a.nQ = 148;
+  a.nK = 148;
+  if (bf16)
+    chunk_skip_kernel<__nv_bfloat16><<<a.nQ + a.nK, 256, 0, st>>>(
+        dkv, reinterpret_cast<__nv_bfloat16*>(dq), reinterpret_cast<__nv_bfloat16*>(dk_own),
+        reinterpret_cast<__nv_bfloat16*>(dv_own), a);
+  else
+    chunk_skip_kernel<float><<<a.nQ + a.nK, 256, 0, st>>>(dkv, reinterpret_cast<float*>(dq),
+                                                          reinterpret_cast<float*>(dk_own),
+                                                          reinterpret_cast<float*>(dv_own), a);
+  return cudaGetLastError();
+}
+
 // ===================================================================== split-KV combine (§8 a9)
 // O = sum_s exp(LSE_s - LSE) O_s,  LSE = log sum_s exp(LSE_s)   (exact merge of softmax partials
 // over disjoint key ranges).  One warp per (head, row); each lane owns 4 of the d = 128 columns.

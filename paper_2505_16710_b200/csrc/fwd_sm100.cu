@@ -62,6 +62,8 @@ struct Args {
   int c, j, hq, G, nqt, nhp;  // chunk size, chunk index, q heads, group size, q tiles, head packs
   int nsplit;                 // split-KV factor (1: final O/LSE written directly)
   int d_out;                  // head dim of the O buffer (64: the D = 128 tile is zero-padded)
+  int wait_prev;              // PDL launch without SECO_FLAG_PREV_INDEPENDENT: wait for the
+                              // predecessor grid before the first global access
   float scale_log2;           // sigma * log2(e)
   int64_t qh, qr;             // o strides (elements)
   float* part_o;              // nsplit > 1: [nsplit][hq][c][D] fp32 normalised partial O
@@ -129,15 +131,27 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   if (warp == 0 && lane == 0) { tma_prefetch(&tm_q); tma_prefetch(&tm_k); tma_prefetch(&tm_v); }
 #if SECO_FWD_PDL
   // Programmatic dependent launch: the next kernel in the stream may start on SMs this grid
-  // leaves idle (its last, partial wave).  Chunk forwards share no data, so a following
-  // forward fills this tail; every other kernel follows a forward with a plain launch.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // leaves idle (its last, partial wave).  A following forward launched with
+  // SECO_FLAG_PREV_INDEPENDENT (the next chunk's forward in stage 1) fills this tail; any
+  // other follower either waits (griddepcontrol.wait) or is a plain launch, which starts
+  // only after this grid completed.  A forward that must wait for its own predecessor
+  // triggers only after that wait (below), so a flagged follower -- which trusts this grid,
+  // not the one before it -- never starts while that earlier kernel may still be writing.
+  if (!a.wait_prev) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
   if (warp == 2) tmem_alloc<L::kTmemCols>(smem_u32(tmem_slot));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#if SECO_FWD_PDL
+  // Without the caller's SECO_FLAG_PREV_INDEPENDENT promise the predecessor may still be
+  // writing Q / K / V (or reading O / LSE): only the prologue above overlaps it.
+  if (a.wait_prev) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -391,6 +405,7 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   a.nqt = g.c / fwd::BM; a.nhp = g.hq / NH;
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.qh = g.qh; a.qr = g.qr; a.d_out = g.d;
+  a.wait_prev = g.prev_indep ? 0 : 1;
   // split-KV (§8 row a9) when the chunk has too few equal-cost units (q tiles x head packs)
   // to fill the SMs -- e.g. head-sharded ranks.  Cost model in K/V-tile units per wave:
   // ~8 tiles of prologue/epilogue per work item, 15% of a unit for the fp32 partial

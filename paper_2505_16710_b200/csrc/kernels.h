@@ -16,7 +16,13 @@ struct ChunkGeom {
   bool det = false;          // SECO_FLAG_DETERMINISTIC: ordered dQ reduction, no Q-split
   int ldq = 0;               // row stride (floats) of the dQ accumulator: 128 on the bf16 path
                              // (d = 64 runs zero-padded to 128), d on the fp32 path
+  bool prev_indep = false;   // SECO_FLAG_PREV_INDEPENDENT: the forward may load before its
+                             // predecessor kernel completes (programmatic dependent launch)
 };
+
+// ---- SpaCO non-sampled chunk (reading Z11): dq = 0, dkv slot j = 0, own copies = 0 ---
+cudaError_t launch_chunk_skip(const ChunkGeom& g, bool bf16, float* dkv, void* dq, void* dk_own, void* dv_own,
+                              cudaStream_t st);
 
 // ---- fp32 debug path (SIMT FFMA, any d <= 256, any c) -------------------------------
 cudaError_t launch_fwd_fp32(const ChunkGeom& g, const float* q, const float* k, const float* v, float* o,

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "kernels.h"
 
@@ -50,34 +51,78 @@ EncodeFn get_encode() {
   return fn;
 }
 
+// ---- tensor-map cache (seco.h "Host-side state").  Encoding is pure host arithmetic on
+// (pointer, sizes, strides, box); a map holds no data, so a cached entry stays exact for any
+// buffer that later occupies the same address with the same geometry.  Bounded: cleared when
+// it reaches kMapCacheMax entries.
+struct MapKey {
+  uintptr_t ptr;
+  int64_t a, b, c, d, e, f, g;   // kind-specific geometry
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e && f == o.f && g == o.g;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ k.ptr;
+    for (int64_t v : {k.a, k.b, k.c, k.d, k.e, k.f, k.g}) h = (h ^ (uint64_t)v) * 0x100000001B3ull + (h >> 29);
+    return (size_t)h;
+  }
+};
+constexpr size_t kMapCacheMax = 4096;
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash>& map_cache() {
+  static auto* m = new std::unordered_map<MapKey, CUtensorMap, MapKeyHash>();
+  return *m;
+}
+template <typename Encode>
+bool cached_map(CUtensorMap* m, const MapKey& key, Encode&& encode) {
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = map_cache().find(key);
+    if (it != map_cache().end()) { *m = it->second; return true; }
+  }
+  if (!encode(m)) return false;
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (map_cache().size() >= kMapCacheMax) map_cache().clear();
+  map_cache().emplace(key, *m);
+  return true;
+}
+
 // 3-D bf16 tensor map over [heads][rows][d], box {64, box_rows, 1}, 128-B swizzle
 bool encode_3d(CUtensorMap* m, const void* ptr, int d, int rows, int heads, int64_t row_stride,
                int64_t head_stride, int box_rows) {
-  EncodeFn enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)heads};
-  cuuint64_t strides[2] = {(cuuint64_t)row_stride * 2, (cuuint64_t)head_stride * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const MapKey key{reinterpret_cast<uintptr_t>(ptr), 3, d, rows, heads, row_stride, head_stride, box_rows};
+  return cached_map(m, key, [&](CUtensorMap* out) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)heads};
+    cuuint64_t strides[2] = {(cuuint64_t)row_stride * 2, (cuuint64_t)head_stride * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  });
 }
 
-// 2-D fp32 tensor map over a dense [rows][128] matrix, box {32, box_rows}, 128-B swizzle
-// (the TMA reduce-add targets: dQ accumulator and dKV)
-// fp32 rows of `cols` floats (boxes of 32 columns; a box past `cols` is skipped by the
-// TMA's bounds check, which is how a zero-padded d = 64 tile reduces into a d = 64 buffer)
+// 2-D fp32 tensor map over a dense [rows][cols] matrix, box {32, box_rows}, 128-B swizzle
+// (the TMA reduce-add targets: dQ accumulator and dKV).  Boxes of 32 columns; a box past
+// `cols` is skipped by the TMA's bounds check, which is how a zero-padded d = 64 tile
+// reduces into a d = 64 buffer.
 bool encode_f32_rows(CUtensorMap* m, const void* ptr, int64_t rows, int box_rows, int cols = 128) {
-  EncodeFn enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const MapKey key{reinterpret_cast<uintptr_t>(ptr), 2, rows, box_rows, cols, 0, 0, 0};
+  return cached_map(m, key, [&](CUtensorMap* out) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  });
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -113,7 +158,8 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
   } else {
     return fail(SECO_ERR_ARG, "unknown dtype %d", (int)s->dtype);
   }
-  if (s->flags & ~SECO_FLAG_DETERMINISTIC) return fail(SECO_ERR_ARG, "unknown flags 0x%x", (unsigned)s->flags);
+  if (s->flags & ~(SECO_FLAG_DETERMINISTIC | SECO_FLAG_PREV_INDEPENDENT))
+    return fail(SECO_ERR_ARG, "unknown flags 0x%x", (unsigned)s->flags);
   return SECO_OK;
 }
 
@@ -127,6 +173,7 @@ seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
   g.scale = s->softmax_scale > 0.f ? s->softmax_scale : 1.0f / std::sqrt((float)s->d);
   g.qh = s->q_head_stride; g.qr = s->q_row_stride; g.kh = s->kv_head_stride; g.kr = s->kv_row_stride;
   g.det = (s->flags & SECO_FLAG_DETERMINISTIC) != 0;
+  g.prev_indep = (s->flags & SECO_FLAG_PREV_INDEPENDENT) != 0;
   g.ldq = dq_ld(s);
   return g;
 }
@@ -249,6 +296,23 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
                              ws_dqacc, ws_D, cs, &launches);
   if (e != cudaSuccess) return cuda_fail(e, "bwd_sm100");
   g_launches = launches;
+  return SECO_OK;
+}
+
+seco_status spaco_chunk_skip(const seco_shape* s, int32_t j, float* dkv, void* dq, void* dk_own, void* dv_own,
+                             seco_stream_t stream) {
+  g_launches = 0;
+  seco_status st = check_shape(s, j);
+  if (st != SECO_OK) return st;
+  if (!dkv || !dq) return fail(SECO_ERR_ARG, "NULL tensor pointer");
+  if (!aligned16(dkv) || (dk_own && !aligned16(dk_own)) || (dv_own && !aligned16(dv_own)))
+    return fail(SECO_ERR_ARG, "dkv / dk_own / dv_own must be 16-byte aligned");
+  if (s->dtype == SECO_BF16 && !aligned16(dq)) return fail(SECO_ERR_ARG, "bf16 tensors must be 16-byte aligned");
+  if (s->d % 4) return fail(SECO_ERR_UNSUPPORTED, "d %% 4 != 0");
+  cudaError_t e = seco::launch_chunk_skip(geom(s, j), s->dtype == SECO_BF16, dkv, dq, dk_own, dv_own,
+                                          reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "chunk_skip");
+  g_launches = 1;
   return SECO_OK;
 }
 

@@ -43,6 +43,7 @@ class _LayerState:
         self.v_cache = torch.zeros(seq, hkv, d, dtype=dtype, device=device)
         self.lse = torch.empty(k, hq, chunk, dtype=torch.float32, device=device)
         self.dkv = torch.zeros(2, hkv, seq, d, dtype=torch.float32, device=device)
+        self.own = torch.empty(2, hkv, chunk, d, dtype=dtype, device=device)    # dk_own / dv_own
         self.shape = _lib.SecoShape(hq, hkv, d, chunk, k, 0.0, _DT[dtype], d, hq * d, d, hkv * d,
                                     _lib.SECO_FLAG_DETERMINISTIC if deterministic else 0)
         self.ws = torch.empty(max(ops.seco_workspace_size(self.shape) // 4, 1), dtype=torch.float32,
@@ -66,14 +67,14 @@ class _ChunkAttention(torch.autograd.Function):
     @staticmethod
     def backward(ctx, do):
         q, o = ctx.saved_tensors
-        st, j, c = ctx.st, ctx.j, ctx.st.chunk
+        st, j = ctx.st, ctx.j
         do = do.contiguous()
         dq = torch.empty_like(q)
         ops.seco_chunk_backward(st.shape, j, q, st.k_cache, st.v_cache, o, do, st.lse[j], ctx.relay, 1.0,
-                                st.dkv, dq, None, None, st.ws)
-        dk = st.dkv[0, :, j * c:(j + 1) * c].transpose(0, 1).to(q.dtype)
-        dv = st.dkv[1, :, j * c:(j + 1) * c].transpose(0, 1).to(q.dtype)
-        return dq, dk, dv, None, None, None
+                                st.dkv, dq, st.own[0], st.own[1], st.ws)
+        # dk_own / dv_own: slot j of dKV after the relay, converted by the library ([hkv][c][d]);
+        # autograd takes them as the gradients of K_j, V_j ([c][hkv][d] views)
+        return dq, st.own[0].transpose(0, 1), st.own[1].transpose(0, 1), None, None, None
 
 
 class _LoRAProj(torch.autograd.Function):
@@ -215,6 +216,12 @@ class ChunkedLoRAStack:
             loss.backward()
             dx0[j * c:(j + 1) * c] = xin.grad
         self._final_chunk = False
+        if not sel:
+            # an empty sample (possible with SPACO_BERNOULLI): no chunk finished any layer, but
+            # every rank must still send every layer's (zero) bucket, top-down like a
+            # non-empty step, or the ranks that did sample chunks would wait forever
+            for li in reversed(range(len(self.params))):
+                self.reducer.layer_final(li, self.buckets[li])
         self.reducer.wait()
         return dx0
 

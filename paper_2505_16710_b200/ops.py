@@ -14,9 +14,11 @@ _DTYPES = {torch.bfloat16: _lib.SECO_BF16, torch.float32: _lib.SECO_FP32_DEBUG}
 
 
 def make_shape(q_full: torch.Tensor, k_cache: torch.Tensor, chunk: int, softmax_scale: float = 0.0,
-               deterministic: bool = False) -> SecoShape:
+               deterministic: bool = False, prev_independent: bool = False) -> SecoShape:
     """Shape record for Q [hq][S][d] (full sequence) and a KV cache [hkv][S][d].
-    deterministic: bit-reproducible backward (SECO_FLAG_DETERMINISTIC)."""
+    deterministic: bit-reproducible backward (SECO_FLAG_DETERMINISTIC).
+    prev_independent: SECO_FLAG_PREV_INDEPENDENT (the caller's promise that the kernel before
+    each forward on the stream neither writes its inputs nor reads its outputs)."""
     if q_full.dtype not in _DTYPES or k_cache.dtype != q_full.dtype:
         raise TypeError("q / k_cache must both be bf16 (tensor-core path) or float32 (debug path)")
     hq, S, d = q_full.shape
@@ -27,7 +29,8 @@ def make_shape(q_full: torch.Tensor, k_cache: torch.Tensor, chunk: int, softmax_
         raise ValueError("sequence length must be a multiple of the chunk size")
     return SecoShape(hq, hkv, d, chunk, S // chunk, float(softmax_scale), _DTYPES[q_full.dtype],
                      q_full.stride(0), q_full.stride(1), k_cache.stride(0), k_cache.stride(1),
-                     _lib.SECO_FLAG_DETERMINISTIC if deterministic else 0)
+                     (_lib.SECO_FLAG_DETERMINISTIC if deterministic else 0)
+                     | (_lib.SECO_FLAG_PREV_INDEPENDENT if prev_independent else 0))
 
 
 def _stream(stream):
@@ -66,6 +69,14 @@ def seco_chunk_backward(shape: SecoShape, j: int, q_j, k_cache, v_cache, o_j, do
     check(lib.seco_chunk_backward(ctypes.byref(shape), j, _p(q_j), _p(k_cache), _p(v_cache), _p(o_j), _p(do_j),
                                   _p(lse_j), float(relay_scale), float(grad_scale), _p(dkv), _p(dq_j),
                                   _p(dk_own), _p(dv_own), _p(ws), wsb, _stream(stream)), "seco_chunk_backward")
+
+
+def spaco_chunk_skip(shape: SecoShape, j: int, dkv, dq_j, dk_own=None, dv_own=None, stream=None):
+    """SpaCO chunk j outside the sample (Alg. 2 line 5; reading Z11): dQ_j = 0, own dK/dV = 0,
+    its checkpoint-gradient slot in dkv dropped (zeroed)."""
+    lib = load()
+    check(lib.spaco_chunk_skip(ctypes.byref(shape), j, _p(dkv), _p(dq_j), _p(dk_own), _p(dv_own), _stream(stream)),
+          "spaco_chunk_skip")
 
 
 def spaco_sample_and_scale(k: int, t: int, seed: int, cap: float = 2.0, mode: int = _lib.SPACO_PAPER):

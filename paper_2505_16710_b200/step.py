@@ -13,6 +13,9 @@ from . import ops
 from .flops import seco_step_flops, spaco_step_flops
 
 
+_CALL_NAMES = {"f": "seco_chunk_forward", "b": "seco_chunk_backward", "z": "spaco_chunk_skip"}
+
+
 @dataclass
 class StepResult:
     selected: list = field(default_factory=list)   # chunk indices processed in stage 2 (descending)
@@ -58,6 +61,11 @@ class ChunkedAttention:
         probe_q = self.o
         probe_k = buf(hkv)
         self.shape = ops.make_shape(probe_q, probe_k, chunk, softmax_scale, deterministic)
+        # stage-1 forwards of chunks j >= 1 follow the previous chunk's forward, which neither
+        # writes their inputs nor reads their outputs: SECO_FLAG_PREV_INDEPENDENT lets each one
+        # start in its predecessor's last wave (programmatic dependent launch)
+        self.shape_chain = ops.make_shape(probe_q, probe_k, chunk, softmax_scale, deterministic,
+                                          prev_independent=True)
         self.ws = torch.empty(max(ops.seco_workspace_size(self.shape) // 4, 1), dtype=torch.float32, device=dev)
 
     # ---- per-chunk calls -------------------------------------------------------------
@@ -68,8 +76,10 @@ class ChunkedAttention:
         """LSE as [hq][S] (a copy)."""
         return self.lse.permute(1, 0, 2).reshape(self.hq, self.seq)
 
-    def forward_chunk(self, q, k_cache, v_cache, j, stream=None):
-        ops.seco_chunk_forward(self.shape, j, ops.chunk_view(q, self.shape, j), k_cache, v_cache,
+    def forward_chunk(self, q, k_cache, v_cache, j, stream=None, chained=False):
+        """chained: the previous kernel on the stream is the previous chunk's stage-1 forward."""
+        shape = self.shape_chain if chained else self.shape
+        ops.seco_chunk_forward(shape, j, ops.chunk_view(q, self.shape, j), k_cache, v_cache,
                                ops.chunk_view(self.o, self.shape, j), self._lse(j), self.ws, stream)
         return ops.last_launch_count()
 
@@ -82,6 +92,50 @@ class ChunkedAttention:
                                 ops.chunk_view(self.dq, self.shape, j), dk_own, dv_own, self.ws, stream)
         return ops.last_launch_count()
 
+    def skip_chunk(self, j, stream=None):
+        """SpaCO chunk outside the sample (reading Z11), at its place in the descending walk."""
+        dk_own = self.own[0] if self.own is not None else None
+        dv_own = self.own[1] if self.own is not None else None
+        ops.spaco_chunk_skip(self.shape, j, self.dkv, ops.chunk_view(self.dq, self.shape, j), dk_own, dv_own,
+                             stream)
+        return ops.last_launch_count()
+
+    def plan(self, selected=None):
+        """The step's chunk calls in the algorithm's order: [("f", j, chained) | ("b", j) |
+        ("z", j)].  Stage 1: forward of every chunk, ascending (Alg. 1/2 lines 1-3).  Stage 2:
+        j = k-1 .. 0; a selected j (default: all) is rebuilt (forward) and backpropagated with
+        the relay (Alg. 1 lines 4-7; Alg. 2 lines 5-8), any other j is skipped (its gradients
+        zero, its checkpoint gradient dropped: reading Z11)."""
+        sel = set(range(self.k)) if selected is None else set(int(i) for i in selected)
+        order = [("f", j, j > 0) for j in range(self.k)]
+        for j in reversed(range(self.k)):
+            order += [("f", j, False), ("b", j)] if j in sel else [("z", j)]
+        return order
+
+    def run(self, order, q, k_cache, v_cache, do, relay_scale=1.0, grad_scale=1.0, stream=None, events=None,
+            nvtx=False):
+        """Issue a plan on one stream (the checkpoint gradients start at zero: dkv is zeroed
+        first).  events: optional per-call (start, end) CUDA event pairs; nvtx: one NVTX range
+        per chunk call (for a profiler timeline).  Returns the number of kernel launches."""
+        self.dkv.zero_()          # checkpoint grads m'.grad start at zero each step (caller-owned buffer)
+        launches = 0
+        for n, op in enumerate(order):
+            if nvtx:
+                torch.cuda.nvtx.range_push(f"{_CALL_NAMES[op[0]]} j={op[1]}")
+            if events is not None:
+                events[n][0].record(stream or torch.cuda.current_stream())
+            if op[0] == "f":
+                launches += self.forward_chunk(q, k_cache, v_cache, op[1], stream, chained=op[2])
+            elif op[0] == "b":
+                launches += self.backward_chunk(q, k_cache, v_cache, do, op[1], relay_scale, grad_scale, stream)
+            else:
+                launches += self.skip_chunk(op[1], stream)
+            if events is not None:
+                events[n][1].record(stream or torch.cuda.current_stream())
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
+        return launches
+
     # ---- whole steps ---------------------------------------------------------------
     def _check(self, q, k_cache, v_cache, do):
         for t, h in ((q, self.hq), (do, self.hq), (k_cache, self.hkv), (v_cache, self.hkv)):
@@ -92,22 +146,12 @@ class ChunkedAttention:
                 raise ValueError(f"inputs must be {self.layout}-laid-out [heads][seq][d] (strides {want})")
 
     def step(self, q, k_cache, v_cache, do, selected=None, relay_scale=1.0, grad_scale=1.0, stream=None):
-        """Stage 1: forward of every chunk, ascending (Alg. 1/2 lines 1-3).
-        Stage 2: for j in `selected` (default: all) descending -- rebuild (forward)
-        then backward with relay (Alg. 1 lines 4-7; Alg. 2 lines 5-8)."""
+        """One SeCO (selected=None) or SpaCO step (selected = the sampled set I): plan() issued
+        on one CUDA stream."""
         self._check(q, k_cache, v_cache, do)
-        sel = list(range(self.k)) if selected is None else sorted(set(int(i) for i in selected))
-        sel = sel[::-1]
+        sel = sorted(set(range(self.k)) if selected is None else set(int(i) for i in selected), reverse=True)
         self.last_selected = sel
-        self.dkv.zero_()          # checkpoint grads m'.grad start at zero each step (caller-owned buffer)
-        if selected is not None:
-            self.dq.zero_()       # rows of non-selected chunks keep dQ = 0 (reading Z11)
-        launches = 0
-        for j in range(self.k):
-            launches += self.forward_chunk(q, k_cache, v_cache, j, stream)
-        for j in sel:
-            launches += self.forward_chunk(q, k_cache, v_cache, j, stream)
-            launches += self.backward_chunk(q, k_cache, v_cache, do, j, relay_scale, grad_scale, stream)
+        launches = self.run(self.plan(selected), q, k_cache, v_cache, do, relay_scale, grad_scale, stream)
         if selected is None:
             fl = seco_step_flops(self.hq, self.d, self.seq, self.chunk)
         else:
@@ -143,9 +187,9 @@ class ChunkedAttention:
 
     @property
     def dk(self):
-        """Gradient of every chunk's own K after the last step (a view of dkv[0]).  For a
-        SpaCO step, slots of non-selected chunks still hold their never-relayed
-        checkpoint gradient; use own_grads() for the per-chunk gradients (zero there)."""
+        """Gradient of every chunk's own K after the last step (a view of dkv[0]): slot j is
+        the total own-chunk gradient after chunk j's relay, and zero for a chunk a SpaCO step
+        skipped (spaco_chunk_skip, reading Z11)."""
         return self.dkv[0]
 
     @property
@@ -153,13 +197,6 @@ class ChunkedAttention:
         return self.dkv[1]
 
     def own_grads(self):
-        """(dK, dV) of each chunk's own K/V after the last step: dkv slots of the chunks
-        processed in stage 2, zero for chunks that were not sampled (reading Z11).
-        Result extraction (a copy), not part of the hot path."""
-        dk, dv = self.dkv[0].clone(), self.dkv[1].clone()
-        sel = set(getattr(self, "last_selected", range(self.k)))
-        for j in range(self.k):
-            if j not in sel:
-                dk[:, j * self.chunk:(j + 1) * self.chunk] = 0
-                dv[:, j * self.chunk:(j + 1) * self.chunk] = 0
-        return dk, dv
+        """(dK, dV) of each chunk's own K/V after the last step (copies of dkv[0], dkv[1]:
+        the library has already zeroed the slots of non-sampled chunks)."""
+        return self.dkv[0].clone(), self.dkv[1].clone()

@@ -100,7 +100,7 @@ def _shape(**kw):
     (dict(q_head_stride=128 * 128), 0, _lib.SECO_ERR_ARG),                  # heads overlap rows
     (dict(q_head_stride=128, q_row_stride=16 * 128), 0, _lib.SECO_ERR_ARG),  # interleaved, too few heads/row
     (dict(kv_head_stride=256 * 128), 0, _lib.SECO_ERR_ARG),                 # cache heads overlap
-    (dict(flags=2), 0, _lib.SECO_ERR_ARG),                                   # unknown flag bit
+    (dict(flags=4), 0, _lib.SECO_ERR_ARG),                                   # unknown flag bit
 ])
 def test_argument_validation(lib, kw, j, code):
     s = _shape(**kw)
@@ -109,6 +109,8 @@ def test_argument_validation(lib, kw, j, code):
     assert r == code, lib.seco_last_error()
     r = lib.seco_chunk_backward(ctypes.byref(s), j, dummy, dummy, dummy, dummy, dummy, dummy, 1.0, 1.0,
                                 dummy, dummy, None, None, dummy, 1 << 30, None)
+    assert r == code, lib.seco_last_error()
+    r = lib.spaco_chunk_skip(ctypes.byref(s), j, dummy, dummy, None, None, None)
     assert r == code, lib.seco_last_error()
 
 
@@ -120,6 +122,10 @@ def test_null_pointers_rejected(lib):
     r = lib.seco_chunk_backward(ctypes.byref(s), 0, dummy, dummy, dummy, dummy, dummy, dummy, 1.0, 1.0,
                                 dummy, dummy, None, None, dummy, 16, None)   # workspace too small
     assert r == _lib.SECO_ERR_ARG
+    assert lib.spaco_chunk_skip(ctypes.byref(s), 0, None, dummy, None, None, None) == _lib.SECO_ERR_ARG
+    assert lib.spaco_chunk_skip(ctypes.byref(s), 0, dummy, None, None, None, None) == _lib.SECO_ERR_ARG
+    misaligned = ctypes.c_void_p((1 << 20) + 4)
+    assert lib.spaco_chunk_skip(ctypes.byref(s), 0, misaligned, dummy, None, None, None) == _lib.SECO_ERR_ARG
 
 
 def test_workspace_size(lib):

@@ -37,3 +37,21 @@ def test_reference_arm_json_line():
     assert line["e2e"] == {"value": line["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["config"]["workload"].startswith("cfg2")
+
+
+def test_bench_gpus_n_spawns_n_ranks_dry_run():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 local ranks
+    (torch.distributed.run); --dry-run takes the same N-rank path on CPU (gloo): head shards,
+    barrier, max-over-ranks time, one JSON line from rank 0."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run",
+                          "--config", "cfg3", "--mode", "spaco", "--sampler", "bernoulli"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(x) for x in out.stdout.strip().splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["dry_run"] and line["n_gpus"] == 2
+    assert line["shards"] == [{"q_heads": [0, 16], "kv_heads": [0, 4]}, {"q_heads": [16, 32], "kv_heads": [4, 8]}]
+    assert line["ms_max_over_ranks"] == 11.0          # rank 1's stand-in time: the max is taken
+    assert line["config"]["parallelism"] == "heads2" and line["config"]["sampler"] == "bernoulli"

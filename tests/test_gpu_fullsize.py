@@ -149,3 +149,75 @@ def test_cfg4_rank_shape_seco_sampled_rows_tail_keys_and_invariants():
     assert np.abs(dk_sum).max() <= BF16_TOL * layer.dk.double().abs().sum(dim=1).max().item()
     do_sum = x.do.astype(np.float64).sum(axis=(0, 1))[None]
     assert err(layer.dv.double().sum(dim=1).cpu().numpy(), do_sum) <= BF16_TOL
+
+
+def _whole_units(c, k, hkv, G):
+    """Number of (call, CTA) work items that take a whole 128-key unit (n0 of the backward work
+    list) over a step's chunk calls, on this GPU's SM count."""
+    import ctypes
+    from paper_2505_16710_b200 import _lib
+    lib = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    out = (ctypes.c_int32 * 4)()
+    return sum((lib.seco_debug_bwd_schedule(c, j, hkv, G, sms, out), out[0])[1] for j in range(k))
+
+
+def _group_ref(x, groups, c, selected=None, gamma=1.0, s=1.0):
+    """Oracle SeCO / SpaCO step of the given kv-head groups (their G q-heads each)."""
+    from oracle import chunkwise as OC
+    qh = [h for g in groups for h in range(g * G_OF(x), (g + 1) * G_OF(x))]
+    sub = (x.q[qh], x.k[groups], x.v[groups], x.do[qh])
+    k = x.q.shape[1] // c
+    if selected is None:
+        return qh, OC.seco_step(*sub, [c] * k)
+    return qh, OC.spaco_step(*sub, [c] * k, selected, gamma, s)
+
+
+def G_OF(x):
+    return x.q.shape[0] // x.k.shape[0]
+
+
+def _compare_groups(layer, ref, qh, groups, what):
+    got = {"o": host(layer.o[qh]), "lse": host(layer.lse_full()[qh]), "dq": host(layer.dq[qh]),
+           "dk": host(layer.dk[groups]), "dv": host(layer.dv[groups])}
+    for name, g in got.items():
+        e = err(g, ref[name])
+        assert e <= BF16_TOL, (what, name, e)
+
+
+def test_cfg2_full_size_elementwise_two_groups():
+    """BASELINE configs[1] (cfg2: 32 q / 8 kv heads, d = 128, 8K tokens, 1K chunks) through the C
+    ABI with every head, then O, LSE, dQ, dK and dV of two whole kv-head groups compared element
+    by element with the oracle (the paper's own check compares every gradient element, App. D
+    P:526).  At this size the backward work list runs whole 128-key units (one CTA owns a
+    cache-slot tile for all of its query tiles, depositing into earlier checkpoints),
+    which the small parity shapes never schedule."""
+    from paper_2505_16710_b200.step import ChunkedAttention
+    hq, hkv, d, s, c = 32, 8, 128, 8192, 1024
+    assert _whole_units(c, s // c, hkv, hq // hkv) > 0
+    x = make_inputs(hq, hkv, s, d, seed=21)
+    q, k, v, do = upload(x, torch.bfloat16)
+    layer = ChunkedAttention(hq, hkv, d, s, c, dtype=torch.bfloat16)
+    layer.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    groups = [2, 7]
+    qh, ref = _group_ref(x, groups, c)
+    _compare_groups(layer, ref, qh, groups, "cfg2 seco")
+    # SpaCO (PAPER mode, t = 3 of 8, cap 2): sampled chunks element-wise, skipped ones zero
+    r = layer.spaco_step(q, k, v, do, 3, 7, cap=2.0, mode=OS.PAPER)
+    torch.cuda.synchronize()
+    qh, ref = _group_ref(x, groups, c, r.selected, r.relay_scale, r.seed_scale)
+    _compare_groups(layer, ref, qh, groups, ("cfg2 spaco", r.selected))
+
+
+def test_cfg3_one_group_every_key(cfg3):
+    """The bench configuration itself (cfg3, 32K tokens, 2K chunks, every head), one kv-head
+    group compared element by element over the whole sequence: O, LSE, dQ of its 4 q heads and
+    dK, dV of every one of its 32768 keys (fp64 oracle, ~5 TFLOP on the host)."""
+    x, (q, k, v, do), layer = cfg3
+    assert _whole_units(C, S // C, HKV, G) > 0
+    layer.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    groups = [3]
+    qh, ref = _group_ref(x, groups, C)
+    _compare_groups(layer, ref, qh, groups, "cfg3 seco group 3")

@@ -27,6 +27,23 @@ def _check_step(layer, ref, tol, selected=None, what=""):
     for name, gpu in (("dq", host(layer.dq)), ("dk", host(dk)), ("dv", host(dv))):
         e = err(gpu, ref[name])
         assert e <= tol, (what, name, e)
+    if layer.own is not None:
+        # dk_own / dv_own (row a7): the element-type copy of slot 0 -- the step's last stage-2
+        # call is chunk 0's backward (or skip) -- against the oracle, and bit-equal to the
+        # round-to-nearest-even conversion of the fp32 slot the library also returns
+        c = layer.chunk
+        for t, name in ((0, "dk"), (1, "dv")):
+            own = layer.own[t]
+            e = err(host(own), ref[name][:, :c])
+            assert e <= tol, (what, name + "_own", e)
+            assert torch.equal(own, layer.dkv[t, :, :c].to(own.dtype)), (what, name + "_own conversion")
+    if selected is not None:
+        # chunks outside the sample (reading Z11): exactly zero, written by spaco_chunk_skip
+        c = layer.chunk
+        for j in range(layer.k):
+            if j not in selected:
+                assert float(layer.dq[:, j * c:(j + 1) * c].abs().max()) == 0.0, (what, j, "dq")
+                assert float(layer.dkv[:, :, j * c:(j + 1) * c].abs().max()) == 0.0, (what, j, "dkv")
 
 
 # ------------------------------------------------------------------ fp32 debug build
@@ -56,14 +73,14 @@ def test_fp32_spaco_step(mode, t):
     hq, hkv, seq, d, c = 2, 1, 64, 16, 16
     x = inputs(hq, hkv, seq, d, seed=2, dtype=torch.float32)
     q, k, v, do = upload(x, torch.float32)
-    layer = _layer(hq, hkv, d, seq, c, torch.float32)
+    layer = _layer(hq, hkv, d, seq, c, torch.float32, own=True)
     for seed in (0, 1, 5):
         r = layer.spaco_step(q, k, v, do, t, seed, cap=0.0, mode=mode)
         torch.cuda.synchronize()
         idx, g, s = OS.sample_and_scale(4, t, seed, 0.0, mode)
         assert r.selected == idx and np.float32(r.relay_scale) == np.float32(g)
         ref = OC.spaco_step(x.q, x.k, x.v, x.do, [c] * 4, idx, g, s)
-        _check_step(layer, ref, FP32_TOL, what=(mode, t, seed))
+        _check_step(layer, ref, FP32_TOL, selected=idx, what=(mode, t, seed))
 
 
 # ------------------------------------------------------------------ bf16 tensor cores
@@ -111,13 +128,13 @@ def test_bf16_spaco_step(t, seed):
     hq, hkv, seq, d, c = 8, 2, 1024, 128, 256
     x = inputs(hq, hkv, seq, d, seed=5)
     q, k, v, do = upload(x, torch.bfloat16)
-    layer = _layer(hq, hkv, d, seq, c, torch.bfloat16)
+    layer = _layer(hq, hkv, d, seq, c, torch.bfloat16, own=True)
     r = layer.spaco_step(q, k, v, do, t, seed, cap=2.0, mode=OS.PAPER)
     torch.cuda.synchronize()
     idx, g, s = OS.sample_and_scale(4, t, seed, 2.0, OS.PAPER)
     assert r.selected == idx
     ref = OC.spaco_step(x.q, x.k, x.v, x.do, [c] * 4, idx, g, s)
-    _check_step(layer, ref, BF16_TOL, what=(t, seed))
+    _check_step(layer, ref, BF16_TOL, selected=idx, what=(t, seed))
 
 
 def test_bf16_chunk_calls_compose():
@@ -279,3 +296,44 @@ print("v1 ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, SECO_BWD_V2="0"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "v1 ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_bf16_forward_waits_for_producer_kernel():
+    """The unsplit forward is a programmatic-dependent launch.  Without
+    SECO_FLAG_PREV_INDEPENDENT it must wait for its predecessor before the first load: a torch
+    copy kernel that writes the K / V cache right before the call is always seen.  With the flag
+    (stage-1 chains, forward after forward) the results are bit-identical to the plain call."""
+    from paper_2505_16710_b200 import ops
+    hq, hkv, seq, d, c = 8, 2, 8192, 128, 2048
+    x = inputs(hq, hkv, seq, d, seed=13)
+    q, k, v, do = upload(x, torch.bfloat16)
+    layer = _layer(hq, hkv, d, seq, c, torch.bfloat16)
+    kc, vc = torch.zeros_like(k), torch.zeros_like(v)
+    big_k = k.repeat(8, 1, 1)                     # a longer producer kernel (8x the cache)
+    sink = torch.empty_like(big_k)
+    j = 3
+    o_ref, lse_ref = OA.chunk_fwd(x.q[:, j * c:(j + 1) * c], x.k, x.v, j * c)
+    qj, oj = ops.chunk_view(q, layer.shape, j), ops.chunk_view(layer.o, layer.shape, j)
+    for rep in range(4):
+        kc.zero_()
+        vc.zero_()
+        torch.cuda.synchronize()
+        sink.copy_(big_k)                         # keeps the GPU busy
+        kc.copy_(k)                               # the producer the forward must wait for
+        vc.copy_(v)
+        ops.seco_chunk_forward(layer.shape, j, qj, kc, vc, oj, layer.lse[j], None)   # ws=None: unsplit, PDL
+        torch.cuda.synchronize()
+        assert err(host(oj), o_ref) <= BF16_TOL, rep
+        assert err(host(layer.lse[j]), lse_ref) <= 1e-4, rep
+    # stage 1 with chained launches == stage 1 with plain launches, bit for bit
+    outs = []
+    for chained in (False, True):
+        layer.o.zero_()
+        for jj in range(seq // c):
+            ops.seco_chunk_forward(layer.shape_chain if (chained and jj > 0) else layer.shape, jj,
+                                   ops.chunk_view(q, layer.shape, jj), k, v,
+                                   ops.chunk_view(layer.o, layer.shape, jj), layer.lse[jj], None)
+        torch.cuda.synchronize()
+        outs.append((layer.o.clone(), layer.lse.clone()))
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    assert torch.equal(outs[0][1].view(torch.int32), outs[1][1].view(torch.int32))
