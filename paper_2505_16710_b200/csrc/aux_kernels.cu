@@ -196,6 +196,7 @@ struct SkipArgs {
   int hq, hkv, c, d, j, S;
   int64_t qh, qr;
   int nQ, nK;
+  int vec;   // 1: dq rows and strides are 16-B aligned (always on the bf16 path) -> 16-B stores
 };
 template <typename T>
 __global__ void __launch_bounds__(256) chunk_skip_kernel(float* __restrict__ dkv, T* __restrict__ dq,
@@ -205,14 +206,21 @@ __global__ void __launch_bounds__(256) chunk_skip_kernel(float* __restrict__ dkv
   const int dv4 = a.d / 4;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   if (bid < a.nQ) {
-    const int64_t total = (int64_t)a.hq * a.c * dv4;
+    constexpr int E = 16 / sizeof(T);          // elements per 16-B store
+    const int per = a.vec ? E : 4;
+    const int dvp = a.d / per;
+    const int64_t total = (int64_t)a.hq * a.c * dvp;
     for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < total; i += (int64_t)a.nQ * blockDim.x) {
-      const int64_t row = i / dv4;
-      const int x = (int)(i - row * dv4) * 4;
+      const int64_t row = i / dvp;
+      const int x = (int)(i - row * dvp) * per;
       const int64_t h = row / a.c, r = row - h * a.c;
-      T* dst = dq + h * a.qh + r * a.qr + x;   // element stores: dq strides need no 16-B alignment
+      T* dst = dq + h * a.qh + r * a.qr + x;
+      if (a.vec) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+      } else {                                  // element stores: fp32 dq strides need no 16-B alignment
 #pragma unroll
-      for (int e = 0; e < 4; ++e) stf(dst + e, 0.f);
+        for (int e = 0; e < 4; ++e) stf(dst + e, 0.f);
+      }
     }
   } else {
     const int64_t per4 = (int64_t)a.c * dv4;
@@ -231,8 +239,11 @@ cudaError_t launch_chunk_skip(const ChunkGeom& g, bool bf16, float* dkv, void* d
   SkipArgs a;
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
   a.qh = g.qh; a.qr = g.qr;
-  a.nQ = 148;
-  a.nK = 148;
+  a.nQ = 296;
+  a.nK = 296;
+  const size_t el = bf16 ? 2 : 4;
+  a.vec = (reinterpret_cast<uintptr_t>(dq) % 16 == 0 && (g.qh * el) % 16 == 0 && (g.qr * el) % 16 == 0 &&
+           (g.d * el) % 16 == 0) ? 1 : 0;
   if (bf16)
     chunk_skip_kernel<__nv_bfloat16><<<a.nQ + a.nK, 256, 0, st>>>(
         dkv, reinterpret_cast<__nv_bfloat16*>(dq), reinterpret_cast<__nv_bfloat16*>(dk_own),

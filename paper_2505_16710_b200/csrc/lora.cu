@@ -11,6 +11,7 @@
 //   cols   a thread owns four columns of X / dY over a contiguous share of the rows (u / t
 //          of those rows staged in smem); per-split partial sums of dA / dB to the workspace
 //   reduce partials added in split order into dA / dB
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "common.cuh"
@@ -202,16 +203,25 @@ __global__ void __launch_bounds__(256) lora_reduce_kernel(const float* __restric
   }
 }
 
+constexpr size_t kColsSmem = 96 * 1024;   // smem cap of lora_cols_kernel (u, t rows of a split)
+
 int lora_splits(const LoraGeom& g) {
   const int col_blocks = (g.n_in + g.n_out + 1023) / 1024;
   int s = (2 * 148 + col_blocks - 1) / col_blocks;
   s = s < 1 ? 1 : s;
   const int max_s = g.rows / 64 > 0 ? g.rows / 64 : 1;   // at least ~64 rows per split
-  return s > max_s ? max_s : s;
+  s = s > max_s ? max_s : s;
+  // the column pass stages u and t of a split's rows in smem: keep that under kColsSmem
+  while ((size_t)2 * ((g.rows + s - 1) / s + 1) * g.rank * 4 > kColsSmem) ++s;
+  return s;
 }
 
+size_t lora_tc_ws_floats(const LoraGeom& g);
+
 size_t lora_ws_floats(const LoraGeom& g) {
-  return (size_t)g.rows * g.rank + (size_t)lora_splits(g) * (g.n_in + g.n_out) * g.rank;
+  const size_t simt = (size_t)g.rows * g.rank + (size_t)lora_splits(g) * (g.n_in + g.n_out) * g.rank;
+  const size_t tc = lora_tc_ws_floats(g);
+  return simt > tc ? simt : tc;
 }
 
 template <typename T, int R>
@@ -230,14 +240,296 @@ static cudaError_t launch_lora_impl(const LoraGeom& g, const void* x, const void
   const int nsplit = lora_splits(g);
   const int max_rows = (g.rows + nsplit - 1) / nsplit + 1;
   auto cols_k = lora_cols_kernel<T, R>;
-  e = cudaFuncSetAttribute(cols_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * max_rows * R * 4);
-  if (e != cudaSuccess) return e;
+  static std::atomic<unsigned long long> attr_done{0};
+  if ((e = ensure_smem_attr(cols_k, (int)kColsSmem, attr_done)) != cudaSuccess) return e;
   dim3 grid((g.n_in + g.n_out + 1023) / 1024, nsplit);
   cols_k<<<grid, 256, (size_t)2 * max_rows * R * 4, st>>>(X, g.ldx, dY, g.ldy, t, u, g.rows, g.n_in, g.n_out, nsplit,
                                                       part);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int rb = ((g.n_in + g.n_out) * R + 255) / 256;
   lora_reduce_kernel<R><<<rb < 296 ? rb : 296, 256, 0, st>>>(part, g.n_in, g.n_out, nsplit, da, db);
+  return cudaGetLastError();
+}
+
+// ============================================================================ bf16 tensor-core path
+// Used when the inputs are bf16 and n_in, n_out are multiples of 256 (every LLaMA projection).
+// The contractions are rank-R skinny GEMMs whose operands are read once from HBM; at R = 8 they
+// are 16 FLOP per loaded element per pass, which the CUDA cores (FFMA, fp32 inputs converted
+// from bf16) cannot sustain at HBM rate, so both passes issue warp-level mma.sync.m16n8k16
+// (bf16 in, fp32 accumulate; N = 8 = R matches the instruction, while a tcgen05 MMA would need
+// N >= 16 and a TMEM round trip for a 16 x 8 result).  Two kernels, each a cluster of 8 CTAs
+// whose partial sums are reduced in a fixed order through distributed shared memory, so the
+// result is deterministic and no partial ever reaches global memory:
+//   tu  : grid (8 column chunks, 64-row blocks, {X.A -> t, dY.B^T -> u}).  A warp owns 4 m16
+//         tiles (64 rows) and k32 steps of its CTA's column chunk; X / dY fragments come from
+//         16-B global loads with the k index permuted inside each 32-column step (thread q owns
+//         physical columns 8q..8q+7; mma 0 takes 8q..8q+3, mma 1 8q+4..8q+7, logical k pairs
+//         (2q, 2q+1) / (2q+8, 2q+9) mapped to consecutive physical pairs), and the same
+//         permutation selects the B fragments (staged in smem in mma order: A columns packed in k
+//         pairs, B rows as loaded).  The 8 chunk partials are summed through DSMEM; the result is
+//         written as fp32 (u_out) and as bf16 hi + lo mma B fragments (x = hi + lo to 2^-16).
+//   grad: grid (8 row splits, 256-column groups of [X | dY]).  dA = X^T u, dB = t^T dY with the
+//         columns of X / dY as M (a thread's 16-B row vectors of 4 rows are re-paired into
+//         k = row fragments with PRMT) and rows as K; hi and lo fragments give two MMAs.  The 8
+//         row-split partials are summed through DSMEM and added into dA / dB.
+// Both kernels read X and dY once each (the second kernel mostly from L2).
+namespace lora_tc {
+constexpr int kCluster = 8;
+constexpr int kThreads = 128;          // 4 warps per CTA
+constexpr int kRowsTU = 64;            // rows per tu CTA (4 m16 tiles per warp)
+constexpr int kColsG = 256;            // columns per grad CTA (64 per warp, 4 m16 tiles)
+
+SECO_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+SECO_DEV uint4 ldg16(const __nv_bfloat16* p, bool ok) {
+  return ok ? __ldg(reinterpret_cast<const uint4*>(p)) : make_uint4(0u, 0u, 0u, 0u);
+}
+// bf16 hi / lo split of two fp32 values (lower k in the low half): x ~= hi + lo
+SECO_DEV void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+  const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
+  const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
+  hi = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+  lo = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+}
+
+struct Args {
+  const __nv_bfloat16 *x, *dy, *a, *b;
+  int64_t ldx, ldy;
+  int rows, n_in, n_out;
+  int nsteps;               // ceil(rows / 16)
+  float *da, *db, *u;       // accumulators, u_out
+  uint4* frag;              // [2 (0: t, 1: u)][nsteps][NT][32] hi/lo B fragments
+};
+
+// ---------------------------------------------------------------- pass 1: t = X A, u = dY B^T
+template <int R>
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
+    lora_tu_kernel(const Args p) {
+  constexpr int NT = (R + 7) / 8, RP = 8 * NT;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int tau = blockIdx.z;                       // 0: X A -> t, 1: dY B^T -> u
+  const int n = tau ? p.n_out : p.n_in;
+  const int chunk = n / kCluster;                   // columns of this CTA (multiple of 32)
+  const int col_c = (int)cluster.block_rank() * chunk;
+  const int row0 = blockIdx.y * kRowsTU;
+  const __nv_bfloat16* M = tau ? p.dy : p.x;
+  const int64_t ld = tau ? p.ldy : p.ldx;
+  // smem: B fragments of the chunk in mma order [k32 step][NT][lane] (16 B each: b0 / b1 of the
+  // step's two mmas) | warp partials [4][64][RP] | CTA partial [64][RP] | one step [16][RP]
+  const int nks = chunk / 32;
+  uint4* sfrag = reinterpret_cast<uint4*>(smem_raw);
+  float* red = reinterpret_cast<float*>(smem_raw + (size_t)nks * NT * 32 * 16);
+  float* part = red + 4 * kRowsTU * RP;
+  float* stepv = part + kRowsTU * RP;
+  // lane (g, q) of step ks, n-tile nt needs the operand at k = 8q..8q+7 of the step, n = 8 nt + g
+  for (int e = threadIdx.x; e < nks * NT * 32; e += kThreads) {
+    const int ln = e % 32, nt = (e / 32) % NT, ks = e / (32 * NT);
+    const int nn = 8 * nt + ln / 4, k0 = col_c + 32 * ks + 8 * (ln % 4);
+    uint4 f = make_uint4(0u, 0u, 0u, 0u);
+    if (nn < R) {
+      if (tau == 0) {   // A [n_in][R]: column nn over 8 consecutive rows, packed in k pairs
+        uint32_t w[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          w[t] = (uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 2 * t) * R + nn]) |
+                 ((uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 2 * t + 1) * R + nn]) << 16);
+        f = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {          // B [R][n_out]: row nn, 8 consecutive columns
+        f = __ldg(reinterpret_cast<const uint4*>(p.b + (int64_t)nn * p.n_out + k0));
+      }
+    }
+    sfrag[e] = f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q = lane % 4;
+  float acc[4][NT][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][nt][e] = 0.f;
+#pragma unroll 2
+  for (int ks = warp; ks < chunk / 32; ks += 4) {
+    const int cl = ks * 32;                         // column of the step within the chunk
+    uint4 xv[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = row0 + 16 * i + g;
+      xv[i][0] = ldg16(M + (int64_t)r * ld + col_c + cl + 8 * q, r < p.rows);
+      xv[i][1] = ldg16(M + (int64_t)(r + 8) * ld + col_c + cl + 8 * q, r + 8 < p.rows);
+    }
+    uint32_t bf[NT][4];     // b0 / b1 of mma 0, b0 / b1 of mma 1
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint4 v = sfrag[(ks * NT + nt) * 32 + lane];
+      bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        mma16816(acc[i][nt], xv[i][0].x, xv[i][1].x, xv[i][0].y, xv[i][1].y, bf[nt][0], bf[nt][1]);
+        mma16816(acc[i][nt], xv[i][0].z, xv[i][1].z, xv[i][0].w, xv[i][1].w, bf[nt][2], bf[nt][3]);
+      }
+  }
+  // warp partials -> smem, summed in warp order
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float* w0 = red + (warp * kRowsTU + 16 * i + g) * RP + 8 * nt + 2 * q;
+      w0[0] = acc[i][nt][0]; w0[1] = acc[i][nt][1];
+      w0[8 * RP] = acc[i][nt][2]; w0[8 * RP + 1] = acc[i][nt][3];
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kRowsTU * RP; e += kThreads)
+    part[e] = red[e] + red[kRowsTU * RP + e] + red[2 * kRowsTU * RP + e] + red[3 * kRowsTU * RP + e];
+  cluster.sync();                                   // every chunk's partial is visible
+  const int rank = (int)cluster.block_rank();
+  if (rank < kRowsTU / 16) {                        // ranks 0..3: one 16-row step each
+    const int step = blockIdx.y * (kRowsTU / 16) + rank;
+    for (int e = threadIdx.x; e < 16 * RP; e += kThreads) {
+      float v = 0.f;
+#pragma unroll
+      for (int c = 0; c < kCluster; ++c) v += cluster.map_shared_rank(part, c)[16 * rank * RP + e];
+      stepv[e] = v;
+      const int r = 16 * step + e / RP, k = e % RP;
+      if (tau == 1 && k < R && r < p.rows) p.u[(int64_t)r * R + k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32 && step < p.nsteps) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int k = 8 * nt + g;
+        uint4 f;
+        split2(stepv[(2 * q) * RP + k], stepv[(2 * q + 1) * RP + k], f.x, f.z);
+        split2(stepv[(2 * q + 8) * RP + k], stepv[(2 * q + 9) * RP + k], f.y, f.w);
+        p.frag[(((int64_t)tau * p.nsteps + step) * NT + nt) * 32 + lane] = f;   // {hi0, hi1, lo0, lo1}
+      }
+    }
+  }
+  cluster.sync();                                   // keep smem alive until every rank has read it
+}
+
+// ---------------------------------------------------------------- pass 2: dA += X^T u, dB += t^T dY
+template <int R>
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
+    lora_grad_kernel(const Args p) {
+  constexpr int NT = (R + 7) / 8, RP = 8 * NT;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ float part[kColsG * RP];
+  const int rank = (int)cluster.block_rank();
+  const int gcol = blockIdx.y * kColsG;             // global column of [X | dY]
+  const bool isA = gcol < p.n_in;
+  const __nv_bfloat16* M = isA ? p.x : p.dy;
+  const int64_t ld = isA ? p.ldx : p.ldy;
+  const int col0 = isA ? gcol : gcol - p.n_in;
+  const uint4* frag = p.frag + (int64_t)(isA ? 1 : 0) * p.nsteps * NT * 32;   // X^T u, t^T dY
+  const int s0 = rank * p.nsteps / kCluster, s1 = (rank + 1) * p.nsteps / kCluster;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q = lane % 4;
+  const int c0 = col0 + 64 * warp + 8 * g;          // this thread's 8 columns
+  float acc[4][NT][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][nt][e] = 0.f;
+#pragma unroll 4
+  for (int s = s0; s < s1; ++s) {
+    const int r = 16 * s + 2 * q;
+    uint4 v[4];
+    v[0] = ldg16(M + (int64_t)r * ld + c0, r < p.rows);
+    v[1] = ldg16(M + (int64_t)(r + 1) * ld + c0, r + 1 < p.rows);
+    v[2] = ldg16(M + (int64_t)(r + 8) * ld + c0, r + 8 < p.rows);
+    v[3] = ldg16(M + (int64_t)(r + 9) * ld + c0, r + 9 < p.rows);
+    uint4 f[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) f[nt] = frag[((int64_t)s * NT + nt) * 32 + lane];
+    const uint32_t* w0 = &v[0].x;
+    const uint32_t* w1 = &v[1].x;
+    const uint32_t* w2 = &v[2].x;
+    const uint32_t* w3 = &v[3].x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t a0 = __byte_perm(w0[j], w1[j], 0x5410), a1 = __byte_perm(w0[j], w1[j], 0x7632);
+      const uint32_t a2 = __byte_perm(w2[j], w3[j], 0x5410), a3 = __byte_perm(w2[j], w3[j], 0x7632);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        mma16816(acc[j][nt], a0, a1, a2, a3, f[nt].x, f[nt].y);   // hi
+        mma16816(acc[j][nt], a0, a1, a2, a3, f[nt].z, f[nt].w);   // lo
+      }
+    }
+  }
+  // CTA partial [256 columns][RP]: tile j, m = g -> column 8g + 2j, m = g + 8 -> 8g + 2j + 1
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float* d0 = part + (64 * warp + 8 * g + 2 * j) * RP + 8 * nt + 2 * q;
+      d0[0] = acc[j][nt][0]; d0[1] = acc[j][nt][1];
+      d0[RP] = acc[j][nt][2]; d0[RP + 1] = acc[j][nt][3];
+    }
+  cluster.sync();
+  // rank r adds columns [32 r, 32 r + 32) of the 8 row-split partials, in rank order
+  for (int e = threadIdx.x; e < 32 * R; e += kThreads) {
+    const int cl = 32 * rank + e / R, k = e % R;
+    float v = 0.f;
+#pragma unroll
+    for (int c = 0; c < kCluster; ++c) v += cluster.map_shared_rank(part, c)[cl * RP + k];
+    if (isA) p.da[(int64_t)(col0 + cl) * R + k] += v;
+    else p.db[(int64_t)k * p.n_out + col0 + cl] += v;
+  }
+  cluster.sync();
+}
+
+template <int R>
+size_t tu_smem(int n_in, int n_out) {
+  constexpr int NT = (R + 7) / 8, RP = 8 * NT;
+  const int nmax = n_in > n_out ? n_in : n_out;
+  return (size_t)(nmax / kCluster / 32) * NT * 32 * 16 + (size_t)(4 * kRowsTU + kRowsTU + 16) * RP * 4;
+}
+}  // namespace lora_tc
+
+bool lora_tc_ok(const LoraGeom& g) {
+  return g.n_in % 256 == 0 && g.n_out % 256 == 0 && g.ldx % 8 == 0 && g.ldy % 8 == 0 &&
+         (g.rank == 1 || g.rank == 2 || g.rank == 4 || g.rank == 8 || g.rank == 16) &&
+         lora_tc::tu_smem<16>(g.n_in, g.n_out) <= 200 * 1024;
+}
+
+size_t lora_tc_ws_floats(const LoraGeom& g) {
+  const int nt = g.rank > 8 ? 2 : 1;
+  return (size_t)2 * ((g.rows + 15) / 16) * nt * 32 * 4;
+}
+
+template <int R>
+static cudaError_t launch_lora_tc(const LoraGeom& g, const void* x, const void* dy, const void* a, const void* b,
+                                  float* da, float* db, float* u, float* ws, cudaStream_t st) {
+  lora_tc::Args p;
+  p.x = static_cast<const __nv_bfloat16*>(x); p.dy = static_cast<const __nv_bfloat16*>(dy);
+  p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
+  p.ldx = g.ldx; p.ldy = g.ldy; p.rows = g.rows; p.n_in = g.n_in; p.n_out = g.n_out;
+  p.nsteps = (g.rows + 15) / 16;
+  p.da = da; p.db = db; p.u = u;
+  p.frag = reinterpret_cast<uint4*>(ws);
+  const size_t smem = lora_tc::tu_smem<R>(g.n_in, g.n_out);
+  static std::atomic<unsigned long long> attr_done{0};
+  cudaError_t e = ensure_smem_attr(lora_tc::lora_tu_kernel<R>, 200 * 1024, attr_done);
+  if (e != cudaSuccess) return e;
+  dim3 g1(lora_tc::kCluster, (g.rows + lora_tc::kRowsTU - 1) / lora_tc::kRowsTU, 2);
+  lora_tc::lora_tu_kernel<R><<<g1, lora_tc::kThreads, smem, st>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  dim3 g2(lora_tc::kCluster, (g.n_in + g.n_out) / lora_tc::kColsG);
+  lora_tc::lora_grad_kernel<R><<<g2, lora_tc::kThreads, 0, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -257,6 +549,16 @@ static cudaError_t launch_lora_t(const LoraGeom& g, const void* x, const void* d
 cudaError_t launch_lora_grad(const LoraGeom& g, bool bf16, const void* x, const void* dy, const void* a,
                              const void* b, float* da, float* db, float* u, float* ws, cudaStream_t st,
                              int* launches) {
+  if (bf16 && lora_tc_ok(g)) {
+    *launches = 2;
+    switch (g.rank) {
+      case 1: return launch_lora_tc<1>(g, x, dy, a, b, da, db, u, ws, st);
+      case 2: return launch_lora_tc<2>(g, x, dy, a, b, da, db, u, ws, st);
+      case 4: return launch_lora_tc<4>(g, x, dy, a, b, da, db, u, ws, st);
+      case 8: return launch_lora_tc<8>(g, x, dy, a, b, da, db, u, ws, st);
+      default: return launch_lora_tc<16>(g, x, dy, a, b, da, db, u, ws, st);
+    }
+  }
   *launches = 4;
   return bf16 ? launch_lora_t<__nv_bfloat16>(g, x, dy, a, b, da, db, u, ws, st)
               : launch_lora_t<float>(g, x, dy, a, b, da, db, u, ws, st);

@@ -117,10 +117,14 @@ def test_bf16_spaco_all_chunks_is_seco():
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-@pytest.mark.parametrize("rows,n_in,n_out,r", [(512, 256, 384, 8), (129, 72, 40, 4), (2048, 1024, 1024, 16)])
+@pytest.mark.parametrize("rows,n_in,n_out,r", [(512, 256, 384, 8), (129, 72, 40, 4), (2048, 1024, 1024, 16),
+                                              (2048, 4096, 1024, 8), (300, 1024, 512, 4), (64, 256, 256, 1),
+                                              (17, 512, 2048, 2)])
 def test_lora_grad_kernel_matches_oracle(dtype, rows, n_in, n_out, r):
     """seco_lora_grad against oracle.multilayer.lora_grads: dA, dB accumulate (two
-    calls give twice the gradient), u = dY B^T; X is a strided view (padded rows)."""
+    calls give twice the gradient), u = dY B^T; X is a strided view (padded rows).  bf16 with
+    n_in, n_out multiples of 256 takes the tensor-core kernels (ragged row counts included),
+    everything else the CUDA-core ones."""
     from paper_2505_16710_b200 import ops
     from synth import round_to_bf16
     rng = np.random.default_rng(rows + r)
