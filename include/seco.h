@@ -212,6 +212,20 @@ int32_t seco_last_launch_count(void);
 int32_t seco_debug_bwd_schedule(int32_t chunk, int32_t j, int32_t hkv, int32_t G, int32_t num_sms,
                                 int32_t* out4);
 
+/* Bounds-check builds (libseco_check.so, compiled with -DSECO_CHECK=1; the stand-in for
+ * compute-sanitizer, which this GPU pool does not offer).  Every kernel asserts its shared-
+ * and tensor-memory operand ranges, mbarrier alignment, TMA box coordinates and global store
+ * indices; a failed assertion is recorded, not trapped.
+ *   seco_debug_check_enabled()   1 in a check build, 0 otherwise (host only).
+ *   seco_debug_check_word()      (failed-check count << 32) | id of the first failed check
+ *                                since the last read, then clears it; synchronises the device
+ *                                (cudaMemcpyFromSymbol); always 0 in a normal build.
+ *   seco_debug_check_selftest()  enqueues one kernel whose check fails (id 999) in a check
+ *                                build, a no-op kernel otherwise. */
+int32_t seco_debug_check_enabled(void);
+uint64_t seco_debug_check_word(void);
+seco_status seco_debug_check_selftest(seco_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,8 @@ SPACO_PAPER, SPACO_HT, SPACO_BERNOULLI = 0, 1, 2
 EXPORTS = ("seco_workspace_size", "seco_chunk_forward", "seco_chunk_backward", "spaco_chunk_skip",
            "spaco_sample_and_scale",
            "seco_lora_workspace_size", "seco_lora_grad",
-           "seco_status_string", "seco_last_error", "seco_last_launch_count", "seco_debug_bwd_schedule")
+           "seco_status_string", "seco_last_error", "seco_last_launch_count", "seco_debug_bwd_schedule",
+           "seco_debug_check_enabled", "seco_debug_check_word", "seco_debug_check_selftest")
 
 
 class SecoShape(ctypes.Structure):
@@ -76,6 +77,13 @@ def load():
     lib.seco_last_error.restype = ctypes.c_char_p
     lib.seco_last_launch_count.argtypes = []
     lib.seco_last_launch_count.restype = i32
+    if hasattr(lib, "seco_debug_check_word"):
+        lib.seco_debug_check_enabled.argtypes = []
+        lib.seco_debug_check_enabled.restype = i32
+        lib.seco_debug_check_word.argtypes = []
+        lib.seco_debug_check_word.restype = ctypes.c_uint64
+        lib.seco_debug_check_selftest.argtypes = [vp]
+        lib.seco_debug_check_selftest.restype = i32
     if hasattr(lib, "seco_debug_bwd_schedule"):      # (older experiment variants lack it)
         lib.seco_debug_bwd_schedule.argtypes = [i32, i32, i32, i32, i32, P(i32)]
         lib.seco_debug_bwd_schedule.restype = i32

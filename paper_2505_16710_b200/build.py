@@ -43,23 +43,26 @@ def _run(cmd, verbose):
         print(r.stdout + r.stderr)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, trace: bool = False,
+          check: bool = False) -> str:
     """Build libseco.so (or, with trace=True, the instrumented libseco_trace.so used by
-    tools/trace_bwd.py; never loaded by the product path)."""
-    global BUILD, LIB
+    tools/trace_bwd.py, or with check=True the bounds-checked libseco_check.so used by
+    tests/test_gpu_check.py; neither is loaded by the product path)."""
+    build_dir, lib = BUILD, LIB
     if trace:
-        BUILD, LIB = BUILD + "_trace", LIB.replace("libseco.so", "libseco_trace.so")
-    # experiment variants: SECO_VARIANT=<name> SECO_DEFINES="-DX=1 ..." -> libseco_<name>.so
-    variant = os.environ.get("SECO_VARIANT")
-    extra = os.environ.get("SECO_DEFINES", "").split()
+        build_dir, lib = build_dir + "_trace", lib.replace("libseco.so", "libseco_trace.so")
+    # experiment variants: SECO_VARIANT=<name> SECO_DEFINES="-DX=1 ..." -> libseco_<name>.so;
+    # check=True builds the bounds-checked libseco_check.so (-DSECO_CHECK=1, common.cuh)
+    variant = "check" if check else os.environ.get("SECO_VARIANT")
+    extra = ["-DSECO_CHECK=1"] if check else os.environ.get("SECO_DEFINES", "").split()
     if variant:
-        BUILD, LIB = BUILD + "_" + variant, LIB.replace("libseco.so", f"libseco_{variant}.so")
-    os.makedirs(BUILD, exist_ok=True)
+        build_dir, lib = build_dir + "_" + variant, lib.replace("libseco.so", f"libseco_{variant}.so")
+    os.makedirs(build_dir, exist_ok=True)
     hdr_t = max(_mtime(h) for h in HEADERS)
     objs = []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
-        op = os.path.join(BUILD, src + ".o")
+        op = os.path.join(build_dir, src + ".o")
         objs.append(op)
         if force or _mtime(op) < max(_mtime(sp), hdr_t):
             flags = CU_FLAGS + (["-Xptxas", "-v"] if ptxas_info else []) + (["-DSECO_TRACE"] if trace else []) + extra
@@ -68,9 +71,9 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, 
             else:
                 cmd = [NVCC] + flags + ["-c", sp, "-o", op]
             _run(cmd, verbose or ptxas_info)
-    if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs, verbose)
-    return LIB
+    if force or _mtime(lib) < max(_mtime(o) for o in objs):
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs, verbose)
+    return lib
 
 
 if __name__ == "__main__":
@@ -79,5 +82,6 @@ if __name__ == "__main__":
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas-info", action="store_true")
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--check", action="store_true", help="bounds-checked libseco_check.so")
     a = ap.parse_args()
-    print(build(a.force, a.verbose, a.ptxas_info, a.trace))
+    print(build(a.force, a.verbose, a.ptxas_info, a.trace, a.check))

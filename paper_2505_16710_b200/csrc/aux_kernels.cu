@@ -185,6 +185,14 @@ cudaError_t launch_final_bf16(const ChunkGeom& g, const float* dqacc, void* dq, 
                                      reinterpret_cast<__nv_bfloat16*>(dv_own), dq_scale, st);
 }
 
+// ===================================================================== SECO_CHECK self-test
+// One failing check (id 999) so a test can see that a check build reports failures.
+__global__ void check_selftest_kernel(int v) { SECO_CHECK_COND(v == 0, 999); }
+cudaError_t launch_check_selftest(cudaStream_t st) {
+  check_selftest_kernel<<<1, 1, 0, st>>>(1);
+  return cudaGetLastError();
+}
+
 // ===================================================================== SpaCO skipped chunk
 // Alg. 2 line 5 ("for i in I") never visits a chunk outside the sample: its dQ, own
 // dK / dV are zero and the deposits later chunks made into its checkpoint slot are dropped
@@ -496,5 +504,7 @@ cudaError_t launch_bwd_fp32(const ChunkGeom& g, const float* q, const float* k, 
   *launches = 3 + ((dk_own || dv_own) ? 1 : 0);
   return e;
 }
+
+unsigned long long check_word_aux() { return seco_check_read_clear(); }
 
 }  // namespace seco

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       // -------------------------------------------------------------- TMA producer
       if (lane == 0) {
         mbar_expect_tx(bar_kv, 2 * kTile);
+        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && g < a.hkv, 410);   // key tile inside slots 0..j
         for (int x = 0; x < D / 64; ++x) {
           tma_load_3d(sK + x * kBox, &tm_k, bar_kv, x * 64, k0, g);
           tma_load_3d(sV + x * kBox, &tm_v, bar_kv, x * 64, k0, g);
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           const int st = i & 1;
           const uint32_t ph = (i >> 1) & 1;
           const int h = g * a.G + w.hh, qt = w.qt;
+          SECO_CHECK_COND(qt * BQ + BQ <= a.c && w.hh < a.G, 411);       // query tile inside chunk j
           // dO first: dP^T(i) is issued before S^T(i), and its buffer frees earlier (dV(i-2))
           mbar_wait(bar_do_empty(st), ph ^ 1);
           mbar_expect_tx(bar_do_full(st), kTile);
@@ -442,6 +444,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       named_bar_sync(2 + mat, 256);
       if ((wg & 1) == 0 && wq == 0 && lane == 0) {
         const int row0 = (mat * a.hkv + g) * a.S + k0;
+        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && row0 + BKV <= 2 * a.hkv * a.S, 510);   // dKV rows
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
         bulk_commit();
@@ -475,6 +478,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
             fence_acq_rel_gpu();
             fence_proxy_async_global();      // ... before this thread's TMA reduce-adds
           }
+          SECO_CHECK_COND(dst >= a.dqacc && dst + 128 * D <= a.dqacc + (int64_t)a.G * a.hkv * a.c * D, 511);
           bulk_reduce_add_f32(dst + 64 * D, dobuf(st), kTile);
           bulk_commit();
           if (!ctr) mbar_wait(bar_stg_half(0), i & 1);
@@ -636,6 +640,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
       // -------------------------------------------------------------- TMA producer
       if (lane == 0) {
         mbar_expect_tx(bar_kv, 2 * kTile);
+        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && g < a.hkv, 410);   // key tile inside slots 0..j
         for (int x = 0; x < D / 64; ++x) {
           tma_load_3d(sK + x * kBox, &tm_k, bar_kv, x * 64, k0, g);
           tma_load_3d(sV + x * kBox, &tm_v, bar_kv, x * 64, k0, g);
@@ -645,6 +650,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
           const int st = i & 1;
           const uint32_t ph = (i >> 1) & 1;
           const int h = g * a.G + w.hh, qt = w.qt;
+          SECO_CHECK_COND(qt * BQ + BQ <= a.c && w.hh < a.G, 412);       // query tile inside chunk j
           mbar_wait(bar_q_empty(st), ph ^ 1);
           mbar_expect_tx(bar_q_full(st), kTile + 2 * BQ * 4);
           for (int x = 0; x < D / 64; ++x)
@@ -746,6 +752,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
           for (int c = 0; c < 4; ++c, ++m) {
             const int s = c & 1;
             mbar_wait(bar_stg_full(s), (m >> 1) & 1);
+            SECO_CHECK_COND(dst >= a.dqacc && dst + 32 * (c + 1) * D <= a.dqacc + (int64_t)a.G * a.hkv * a.c * D, 512);
             bulk_reduce_add_f32(dst + 32 * c * D, sSTG + s * kSlot, kSlot);
             bulk_commit();
             if (c == 0) V2TRACE(16, i);
@@ -924,6 +931,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
       named_bar_sync(2 + mat, 128);
       if (wq == 0 && lane == 0) {
         const int row0 = (mat * a.hkv + g) * a.S + k0;
+        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && row0 + BKV <= 2 * a.hkv * a.S, 510);   // dKV rows
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
         bulk_commit();
@@ -1114,5 +1122,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   *launches = 2 + 1;
   return e;
 }
+
+unsigned long long check_word_bwd() { return seco_check_read_clear(); }
 
 }  // namespace seco

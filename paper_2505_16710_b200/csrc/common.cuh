@@ -11,7 +11,59 @@
 
 #define SECO_DEV __device__ __forceinline__
 
+// ---------------------------------------------------------------- SECO_CHECK builds
+// compute-sanitizer is closed on this pool, so the bounds it would check are
+// asserted in-kernel by a separate build (libseco_check.so: -DSECO_CHECK=1, see build.py):
+// shared-memory operands and TMA destinations inside the CTA's shared window, tensor-memory
+// columns inside the allocation and lanes inside the issuing warp's sub-partition, mbarrier
+// alignment, TMA box coordinates inside the tensor, and plain global stores inside their
+// buffers (call sites).  A failed check records its id (first failure) and a count in a
+// per-translation-unit device word that the host reads through seco_debug_check_word(); the
+// kernel carries on, so a failure is reported after the call instead of ending the context.
+#ifdef SECO_CHECK
+static __device__ unsigned int g_seco_check[2];     // [0] first failing check id, [1] count
+#define SECO_CHECK_COND(cond, id)                                   \
+  do {                                                              \
+    if (!(cond)) {                                                  \
+      atomicCAS(&g_seco_check[0], 0u, (unsigned)(id));              \
+      atomicAdd(&g_seco_check[1], 1u);                              \
+    }                                                               \
+  } while (0)
+// host: read and clear this translation unit's check word ((count << 32) | first id)
+static inline unsigned long long seco_check_read_clear() {
+  unsigned int w[2] = {0u, 0u}, z[2] = {0u, 0u};
+  cudaMemcpyFromSymbol(w, g_seco_check, sizeof(w));
+  cudaMemcpyToSymbol(g_seco_check, z, sizeof(z));
+  return ((unsigned long long)w[1] << 32) | w[0];
+}
+#else
+#define SECO_CHECK_COND(cond, id) \
+  do {                            \
+  } while (0)
+static inline unsigned long long seco_check_read_clear() { return 0ull; }
+#endif
+// check ids: 1xx smem, 2xx tmem, 3xx mbarrier, 4xx TMA coordinates, 5xx global stores
+
 namespace seco {
+
+#ifdef SECO_CHECK
+__device__ __forceinline__ uint32_t total_smem_bytes() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%total_smem_size;" : "=r"(v));
+  return v;
+}
+#define SECO_CHECK_SMEM(addr, bytes, id) \
+  SECO_CHECK_COND((uint64_t)(addr) + (uint64_t)(bytes) <= (uint64_t)::seco::total_smem_bytes(), id)
+// TMEM address: lane in bits 31:16, column in 15:0; allocations here are at most 512 columns
+// and a warp's tcgen05.ld / st reach only the 32 lanes of its sub-partition (warp id % 4)
+#define SECO_CHECK_TMEM_COLS(taddr, ncols, id) SECO_CHECK_COND(((taddr) & 0xFFFFu) + (ncols) <= 512u, id)
+#define SECO_CHECK_TMEM_WARP(taddr, id) \
+  SECO_CHECK_COND(((taddr) >> 16) == 32u * ((threadIdx.x / 32u) % 4u), id)
+#else
+#define SECO_CHECK_SMEM(addr, bytes, id) SECO_CHECK_COND(true, id)
+#define SECO_CHECK_TMEM_COLS(taddr, ncols, id) SECO_CHECK_COND(true, id)
+#define SECO_CHECK_TMEM_WARP(taddr, id) SECO_CHECK_COND(true, id)
+#endif
 
 SECO_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -19,6 +71,8 @@ SECO_DEV uint32_t smem_u32(const void* p) {
 
 // ---------------------------------------------------------------- mbarrier
 SECO_DEV void mbar_init(uint32_t bar, uint32_t count) {
+  SECO_CHECK_COND((bar & 7u) == 0u, 301);
+  SECO_CHECK_SMEM(bar, 8, 302);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 SECO_DEV void fence_barrier_init() {
@@ -28,6 +82,7 @@ SECO_DEV void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 SECO_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  SECO_CHECK_SMEM(bar, 8, 303);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
@@ -58,7 +113,11 @@ SECO_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
 SECO_DEV void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
+// every 3-D map here has a {64, 128, 1} box of bf16 (16 KiB) with the 128-B swizzle (1024-B aligned)
 SECO_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
+  SECO_CHECK_SMEM(dst, 16384, 101);
+  SECO_CHECK_COND((dst & 1023u) == 0u, 102);
+  SECO_CHECK_COND(c0 >= 0 && c1 >= 0 && c2 >= 0 && (c0 & 63) == 0, 401);
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
@@ -66,6 +125,8 @@ SECO_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int 
       : "memory");
 }
 SECO_DEV void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  SECO_CHECK_SMEM(dst, bytes, 103);
+  SECO_CHECK_COND((dst & 15u) == 0u && (bytes & 15u) == 0u, 104);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
@@ -91,7 +152,13 @@ SECO_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_syn
 SECO_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // D[tmem] (+)= A[smem desc] * B[smem desc]^T  (kind::f16, fp32 accumulate)
+// descriptor start address (bits 13:0, units of 16 B): an operand tile of up to 32 KiB in the window
+#define SECO_CHECK_DESC(desc, id) SECO_CHECK_SMEM(((uint32_t)(desc) & 0x3FFFu) << 4, 16 * 128, id)
 SECO_DEV void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  SECO_CHECK_TMEM_COLS(d_tmem, (idesc >> 17 & 0x3Fu) << 3, 201);
+  SECO_CHECK_COND((d_tmem >> 16) == 0u, 202);
+  SECO_CHECK_DESC(a_desc, 105);
+  SECO_CHECK_DESC(b_desc, 106);
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -101,6 +168,10 @@ SECO_DEV void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t
 }
 // D[tmem] (+)= A[tmem] * B[smem desc]^T  (A in tensor memory: lane = row, 2 bf16 per column)
 SECO_DEV void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  SECO_CHECK_TMEM_COLS(d_tmem, (idesc >> 17 & 0x3Fu) << 3, 203);
+  SECO_CHECK_TMEM_COLS(a_tmem, 8, 204);
+  SECO_CHECK_COND((d_tmem >> 16) == 0u && (a_tmem >> 16) == 0u, 205);
+  SECO_CHECK_DESC(b_desc, 107);
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -110,6 +181,7 @@ SECO_DEV void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t
 }
 // arrive (once) on an mbarrier when all previously issued tcgen05.mma of this thread complete
 SECO_DEV void mma_commit(uint32_t bar) {
+  SECO_CHECK_SMEM(bar, 8, 304);
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
@@ -127,6 +199,8 @@ SECO_DEV void mma_commit(uint32_t bar) {
 
 // 32 consecutive fp32 columns of this thread's TMEM lane (warp w reads lanes 32*(w%4)..+31)
 SECO_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  SECO_CHECK_TMEM_COLS(taddr, 32u, 210);
+  SECO_CHECK_TMEM_WARP(taddr, 211);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
       "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
@@ -135,6 +209,8 @@ SECO_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 SECO_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  SECO_CHECK_TMEM_COLS(taddr, 32u, 212);
+  SECO_CHECK_TMEM_WARP(taddr, 213);
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
       "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, "
@@ -143,6 +219,8 @@ SECO_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 SECO_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  SECO_CHECK_TMEM_COLS(taddr, 16u, 214);
+  SECO_CHECK_TMEM_WARP(taddr, 215);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
       "%15}, [%16];"
@@ -151,16 +229,22 @@ SECO_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 SECO_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  SECO_CHECK_TMEM_COLS(taddr, 8u, 216);
+  SECO_CHECK_TMEM_WARP(taddr, 217);
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
 SECO_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  SECO_CHECK_TMEM_COLS(taddr, 8u, 218);
+  SECO_CHECK_TMEM_WARP(taddr, 219);
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
 SECO_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  SECO_CHECK_TMEM_COLS(taddr, 16u, 220);
+  SECO_CHECK_TMEM_WARP(taddr, 221);
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
       "%13, %14, %15, %16};" ::"r"(taddr),

@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      SECO_CHECK_COND(qt * fwd::BM + fwd::BM <= a.c && h0 + NH <= a.hq, 420);    // query tile inside chunk j
+      SECO_CHECK_COND(t0 >= 0 && (t0 + nT) * fwd::BN <= (a.j + 1) * a.c, 421);    // key tiles inside slots 0..j
       for (int b = 0; b < NH; ++b) {
         mbar_expect_tx(bar_q(b), L::kTileBytes);
         for (int x = 0; x < HALVES; ++x)
@@ -356,9 +358,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           dst[q] = w;
         }
       }
+      SECO_CHECK_COND(h < a.hq && qt * fwd::BM + r < a.c, 520);
       lse[(int64_t)h * a.c + qt * fwd::BM + r] = lse_v;
     } else {
       const int64_t prow = ((int64_t)split * a.hq + h) * a.c + qt * fwd::BM + r;
+      SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.c, 521);
       float4* dst = reinterpret_cast<float4*>(a.part_o + prow * D);
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
@@ -478,5 +482,7 @@ cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   }
   return cudaErrorInvalidValue;
 }
+
+unsigned long long check_word_fwd() { return seco_check_read_clear(); }
 
 }  // namespace seco

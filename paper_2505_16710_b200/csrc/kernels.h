@@ -20,6 +20,13 @@ struct ChunkGeom {
                              // predecessor kernel completes (programmatic dependent launch)
 };
 
+// ---- SECO_CHECK builds (common.cuh): per-translation-unit check words, read and cleared ----
+unsigned long long check_word_fwd();
+unsigned long long check_word_bwd();
+unsigned long long check_word_aux();
+unsigned long long check_word_lora();
+cudaError_t launch_check_selftest(cudaStream_t st);
+
 // ---- SpaCO non-sampled chunk (reading Z11): dq = 0, dkv slot j = 0, own copies = 0 ---
 cudaError_t launch_chunk_skip(const ChunkGeom& g, bool bf16, float* dkv, void* dq, void* dk_own, void* dv_own,
                               cudaStream_t st);

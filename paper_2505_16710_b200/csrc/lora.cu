@@ -564,4 +564,6 @@ cudaError_t launch_lora_grad(const LoraGeom& g, bool bf16, const void* x, const 
               : launch_lora_t<float>(g, x, dy, a, b, da, db, u, ws, st);
 }
 
+unsigned long long check_word_lora() { return seco_check_read_clear(); }
+
 }  // namespace seco

@@ -316,6 +316,30 @@ seco_status spaco_chunk_skip(const seco_shape* s, int32_t j, float* dkv, void* d
   return SECO_OK;
 }
 
+uint64_t seco_debug_check_word(void) {
+  const unsigned long long w[4] = {seco::check_word_fwd(), seco::check_word_bwd(), seco::check_word_aux(),
+                                   seco::check_word_lora()};
+  uint64_t count = 0, first = 0;
+  for (unsigned long long x : w) {
+    count += x >> 32;
+    if (!first) first = x & 0xFFFFFFFFull;
+  }
+  return (count << 32) | first;
+}
+
+int32_t seco_debug_check_enabled(void) {
+#ifdef SECO_CHECK
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+seco_status seco_debug_check_selftest(seco_stream_t stream) {
+  cudaError_t e = seco::launch_check_selftest(reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SECO_OK : cuda_fail(e, "check_selftest");
+}
+
 static bool lora_geom(const seco_lora_shape* s, seco::LoraGeom* g) {
   if (!s || s->rows <= 0 || s->n_in <= 0 || s->n_out <= 0 || s->rank <= 0) return false;
   g->rows = s->rows; g->n_in = s->n_in; g->n_out = s->n_out; g->rank = s->rank;

@@ -217,3 +217,8 @@ def test_bwd_work_list_covers_every_block_once(lib, c, k, hkv, G):
             for (a0, a1, _), (b0, b1, _) in zip(rs, rs[1:]):
                 assert a1 == b0 and a0 <= a1
         assert grid >= n_units
+
+
+def test_normal_build_has_no_checks(lib):
+    """The product libseco.so is not the bounds-checked build (tests/test_gpu_check.py runs that)."""
+    assert lib.seco_debug_check_enabled() == 0
