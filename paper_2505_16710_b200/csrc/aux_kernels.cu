@@ -35,6 +35,7 @@ struct PrepArgs {
   int ldq;         // dQacc row stride (floats)
   int* order;      // deterministic mode: dQ order counters [hq][c/128] to zero (else null)
   int n_order;
+  int vec;         // Task A on 16-B vectors (bf16, d in {64, 128}; nD is then a grid-stride count)
 };
 
 // Task A (blocks [0,nD)): one warp per (h, row): D = sum_x dO*O (and -LSE log2 e for the
@@ -47,7 +48,45 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
                                                        float* __restrict__ dqacc, const float* __restrict__ lse,
                                                        float* __restrict__ nlse, PrepArgs a) {
   const int bid = blockIdx.x;
-  if (bid < a.nD) {
+  if (bid < a.nD && a.vec) {
+    // bf16 rows of d in {64, 128} (16-B aligned, checked by the ABI): d/8 lanes per row, one
+    // 16-B load of O and of dO per lane, 4 row groups of a warp in flight per step (grid-stride)
+    const int lpr = a.d / 8, rpw = 32 / lpr;
+    const int lane = threadIdx.x % 32, sub = lane / lpr, x = (lane % lpr) * 8;
+    const int nrows = a.hq * a.c;
+    const int gw = bid * 8 + threadIdx.x / 32, nw = a.nD * 8;
+    constexpr int B = 4;
+    for (int w0 = gw * rpw * B; w0 < nrows; w0 += nw * rpw * B) {
+      uint4 ov[B], dv[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int w = w0 + u * rpw + sub;
+        if (w < nrows) {
+          const int h = w / a.c, r = w % a.c;
+          ov[u] = *reinterpret_cast<const uint4*>(o + (int64_t)h * a.qh + (int64_t)r * a.qr + x);
+          dv[u] = *reinterpret_cast<const uint4*>(d_o + (int64_t)h * a.qh + (int64_t)r * a.qr + x);
+        } else {
+          ov[u] = dv[u] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const uint32_t* op = &ov[u].x;
+        const uint32_t* dp = &dv[u].x;
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          acc += __uint_as_float(op[e] << 16) * __uint_as_float(dp[e] << 16) +
+                 __uint_as_float(op[e] & 0xffff0000u) * __uint_as_float(dp[e] & 0xffff0000u);
+        for (int off = lpr / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        const int w = w0 + u * rpw + sub;
+        if (lane % lpr == 0 && w < nrows) {
+          D[w] = acc;
+          if (nlse) nlse[w] = -1.4426950408889634f * lse[w];
+        }
+      }
+    }
+  } else if (bid < a.nD) {
     const int w = bid * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (w >= a.hq * a.c) return;
     const int h = w / a.c, r = w % a.c;
@@ -147,7 +186,8 @@ static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, flo
   PrepArgs a;
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
   a.qh = g.qh; a.qr = g.qr; a.relay = relay;
-  a.nD = (g.hq * g.c + 7) / 8;
+  a.vec = (sizeof(T) == 2 && (g.d == 64 || g.d == 128)) ? 1 : 0;
+  a.nD = a.vec ? 296 : (g.hq * g.c + 7) / 8;
   a.nR = relay == 1.f ? 0 : 296;
   a.nZ = dqacc ? 296 : 0;
   a.order = order;

@@ -47,13 +47,16 @@ static inline unsigned long long seco_check_read_clear() { return 0ull; }
 namespace seco {
 
 #ifdef SECO_CHECK
-__device__ __forceinline__ uint32_t total_smem_bytes() {
-  uint32_t v;
-  asm volatile("mov.u32 %0, %%total_smem_size;" : "=r"(v));
-  return v;
+// end of this CTA's shared window: the dynamic block follows any static shared data, so its
+// base (every extern __shared__ array aliases it) plus %dynamic_smem_size is the window's end
+__device__ __forceinline__ uint32_t smem_window_end() {
+  extern __shared__ __align__(16) uint8_t seco_check_dyn_smem[];
+  uint32_t dyn;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  return static_cast<uint32_t>(__cvta_generic_to_shared(seco_check_dyn_smem)) + dyn;
 }
 #define SECO_CHECK_SMEM(addr, bytes, id) \
-  SECO_CHECK_COND((uint64_t)(addr) + (uint64_t)(bytes) <= (uint64_t)::seco::total_smem_bytes(), id)
+  SECO_CHECK_COND((uint64_t)(addr) + (uint64_t)(bytes) <= (uint64_t)::seco::smem_window_end(), id)
 // TMEM address: lane in bits 31:16, column in 15:0; allocations here are at most 512 columns
 // and a warp's tcgen05.ld / st reach only the 32 lanes of its sub-partition (warp id % 4)
 #define SECO_CHECK_TMEM_COLS(taddr, ncols, id) SECO_CHECK_COND(((taddr) & 0xFFFFu) + (ncols) <= 512u, id)
@@ -113,9 +116,11 @@ SECO_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
 SECO_DEV void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
-// every 3-D map here has a {64, 128, 1} box of bf16 (16 KiB) with the 128-B swizzle (1024-B aligned)
-SECO_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
-  SECO_CHECK_SMEM(dst, 16384, 101);
+// 3-D maps have a {64, rows, 1} box of bf16 (rows = 128: 16 KiB; the pair forward's K halves use
+// 64-row boxes) with the 128-B swizzle (1024-B aligned)
+SECO_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2,
+                          uint32_t box_bytes = 16384) {
+  SECO_CHECK_SMEM(dst, box_bytes, 101);
   SECO_CHECK_COND((dst & 1023u) == 0u, 102);
   SECO_CHECK_COND(c0 >= 0 && c1 >= 0 && c2 >= 0 && (c0 & 63) == 0, 401);
   asm volatile(
@@ -124,6 +129,60 @@ SECO_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// ---------------------------------------------------------------- CTA pairs (cluster of 2)
+// The pair forward (fwd_sm100.cu) issues tcgen05.mma.cta_group::2 from the leader
+// (rank 0) on both CTAs' operands and TMEM; TMA loads of either CTA complete on the leader's
+// barriers; the leader's commits arrive on both CTAs' barriers (multicast).
+SECO_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared::cta offset in CTA `rank` of the cluster
+SECO_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+SECO_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+SECO_DEV void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+SECO_DEV void mbar_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster),
+               "r"(bytes)
+               : "memory");
+}
+SECO_DEV bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+SECO_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait_cluster(bar, parity)) {
+  }
+}
+// TMA load into this CTA's smem whose completion is counted on a barrier of either CTA of the pair
+SECO_DEV void tma_load_3d_pair(uint32_t dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1, int c2,
+                               uint32_t box_bytes) {
+  SECO_CHECK_SMEM(dst, box_bytes, 108);
+  SECO_CHECK_COND((dst & 1023u) == 0u, 109);
+  SECO_CHECK_COND(c0 >= 0 && c1 >= 0 && c2 >= 0 && (c0 & 63) == 0, 402);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes.cta_group::2"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 SECO_DEV void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   SECO_CHECK_SMEM(dst, bytes, 103);
   SECO_CHECK_COND((dst & 15u) == 0u && (bytes & 15u) == 0u, 104);
@@ -147,6 +206,17 @@ template <int NCOLS>
 SECO_DEV void tmem_dealloc(uint32_t taddr) {  // whole warp
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS)
                : "memory");
+}
+template <int NCOLS>
+SECO_DEV void tmem_alloc_pair(uint32_t dst_smem) {  // whole warp, in both CTAs of the pair
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+SECO_DEV void tmem_dealloc_pair(uint32_t taddr) {  // whole warp, in both CTAs of the pair
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
 }
 SECO_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 SECO_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -179,6 +249,40 @@ SECO_DEV void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// pair MMAs (issued by the leader CTA only): M = 256 rows, 128 from each CTA's A operand (smem
+// descriptor or TMEM at the same address in both), B's N columns split between the two CTAs'
+// smem at the same offset; D lands in each CTA's TMEM (its own 128 rows, all N columns)
+SECO_DEV void mma_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  SECO_CHECK_TMEM_COLS(d_tmem, (idesc >> 17 & 0x3Fu) << 3, 206);
+  SECO_CHECK_DESC(a_desc, 110);
+  SECO_CHECK_DESC(b_desc, 111);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+SECO_DEV void mma_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  SECO_CHECK_TMEM_COLS(d_tmem, (idesc >> 17 & 0x3Fu) << 3, 207);
+  SECO_CHECK_TMEM_COLS(a_tmem, 8, 208);
+  SECO_CHECK_DESC(b_desc, 112);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the leader's MMAs complete
+SECO_DEV void mma_commit_pair(uint32_t bar) {
+  SECO_CHECK_SMEM(bar, 8, 305);
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 // arrive (once) on an mbarrier when all previously issued tcgen05.mma of this thread complete
 SECO_DEV void mma_commit(uint32_t bar) {
   SECO_CHECK_SMEM(bar, 8, 304);

@@ -18,6 +18,7 @@
 // so the softmax of one tile overlaps tensor-core work of the other.  S_b(t+1) may
 // overwrite P_b(t) because tcgen05.mma from one thread executes in issue order.
 // TMEM: S_b / P_b at columns [128b, 128b+128), O_b at [128 NH + D b, ... + D).
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -389,16 +390,335 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
 #endif
 }
 
+// ============================================================================ CTA-pair forward
+// seco_fwd2_sm100_kernel: the same algorithm as seco_fwd_sm100_kernel (NH = 2 heads per CTA,
+// single-pass online softmax, P in TMEM, lazy rescale, ping-pong MMA order), issued as
+// tcgen05.mma.cta_group::2 on a cluster of 2 CTAs.  The pair covers one 128-row query tile of
+// the 4 q-heads of one kv-head group (CTA r: heads 4 quad + 2 r, +1), so both CTAs see the same
+// K/V tiles and the same causal mask.  Per K/V tile each CTA loads only half of K (keys
+// [64 r, 64 r + 64), all d: the N half of S's B operand) and half of V (all keys, d columns
+// [64 r, 64 r + 64): the N half of PV's B operand), and each M = 256 MMA reads only that half
+// from each CTA's shared memory: per CTA and K/V tile 2 x 48 KiB of S operands + 2 x 16 KiB of
+// PV operands + 32 KiB of TMA writes, against 2 x 64 + 2 x 32 + 64 KiB unpaired -- the
+// unpaired kernel's shared-memory port was ~98 % busy.
+// Roles: the leader's warp 1 issues every MMA of the pair; the producers of both CTAs load into
+// their own smem and complete on the leader's q / kv_full barriers (TMA .cta_group::2); the
+// leader's commits arrive on both CTAs' s_full / o_full / kv_empty (multicast); both CTAs'
+// softmax warps arrive on the leader's p_half barriers (8 arrivals: 4 warps x 2 CTAs).
+namespace fwd2 {
+constexpr int NH = 2, D = 128, BM = 128, BN = 128;
+constexpr int kQBytes = BM * D * 2;                  // one head's Q tile (32 KiB)
+constexpr int kStage = 64 * D * 2;                   // a K half or a V half (16 KiB)
+template <int STAGES>
+struct Layout {
+  static constexpr int kQ = 0;
+  static constexpr int kKV = kQ + NH * kQBytes;
+  static constexpr int kBar = kKV + STAGES * kStage;
+  // barriers: q[NH], kv_full[STAGES], kv_empty[STAGES], s_full[NH], p_half[NH][2], o_full[NH]
+  static constexpr int kNumBars = NH + 2 * STAGES + 4 * NH;
+  static constexpr int kTmemSlot = kBar + 8 * kNumBars;
+  static constexpr int kBytes = kTmemSlot + 16;
+  static constexpr int kAlloc = kBytes + 1024;
+  static constexpr int kThreads = 128 + 128 * NH;
+};
+}  // namespace fwd2
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>::kThreads, 1)
+    seco_fwd2_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
+                           float* __restrict__ lse, const fwd::Args a) {
+  using namespace fwd2;
+  using L = Layout<STAGES>;
+  constexpr int BOX = 128 * 128;                     // one [128 rows][128 B] box (Q)
+  constexpr int HBOX = 64 * 128;                     // one [64 rows][128 B] box (K half)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sQ = sbase + L::kQ, sKV = sbase + L::kKV;
+  const uint32_t bar0 = sbase + L::kBar;
+  auto bar_q = [&](int b) { return bar0 + 8u * b; };
+  auto bar_kv_full = [&](int s) { return bar0 + 8u * (NH + s); };
+  auto bar_kv_empty = [&](int s) { return bar0 + 8u * (NH + STAGES + s); };
+  auto bar_s_full = [&](int b) { return bar0 + 8u * (NH + 2 * STAGES + b); };
+  auto bar_p_half = [&](int b, int hf) { return bar0 + 8u * (2 * NH + 2 * STAGES + 2 * b + hf); };
+  auto bar_o_full = [&](int b) { return bar0 + 8u * (4 * NH + 2 * STAGES + b); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  // heavier query tiles first; split-KV part innermost; the pair shares (query tile, head quad)
+  const int pair = (int)blockIdx.x / 2;
+  const int unit = pair / a.nsplit, split = pair % a.nsplit;
+  const int nquad = a.hq / 4;
+  const int qt = a.nqt - 1 - unit / nquad;
+  const int quad = unit % nquad;
+  const int h0 = quad * 4 + 2 * (int)rank, g = (quad * 4) / a.G;
+  const int q0 = a.j * a.c + qt * BM;
+  const int T = q0 / BN + 1;
+  const int t0 = T * split / a.nsplit;
+  const int nT = T * (split + 1) / a.nsplit - t0;
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NH; ++b) mbar_init(bar_q(b), 1);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(bar_kv_full(s), 1); mbar_init(bar_kv_empty(s), 1); }
+    for (int b = 0; b < NH; ++b) {
+      mbar_init(bar_s_full(b), 1);
+      mbar_init(bar_p_half(b, 0), 8);                // 4 softmax warps of each CTA (leader's copy)
+      mbar_init(bar_p_half(b, 1), 8);
+      mbar_init(bar_o_full(b), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tm_q); tma_prefetch(&tm_k); tma_prefetch(&tm_v); }
+#if SECO_FWD_PDL
+  if (!a.wait_prev) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  if (warp == 2) tmem_alloc_pair<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                                    // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+#if SECO_FWD_PDL
+  if (a.wait_prev) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+#endif
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      SECO_CHECK_COND(qt * BM + BM <= a.c && h0 + NH <= a.hq, 422);
+      SECO_CHECK_COND(t0 >= 0 && (t0 + nT) * BN <= (a.j + 1) * a.c, 423);
+      for (int b = 0; b < NH; ++b) {
+        if (leader) mbar_expect_tx(bar_q(b), 2 * kQBytes);     // both CTAs' Q_b
+        const uint32_t bq = mapa_shared(bar_q(b), 0);
+        for (int x = 0; x < 2; ++x)
+          tma_load_3d_pair(sQ + b * kQBytes + x * BOX, &tm_q, bq, x * 64, qt * BM, h0 + b, BOX);
+      }
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int t = t0; t < t0 + nT; ++t) {
+        for (int w = 0; w < 2; ++w) {  // K_t half then V_t half
+          mbar_wait(bar_kv_empty(slot), phase ^ 1);
+          if (leader) mbar_expect_tx(bar_kv_full(slot), 2 * kStage);
+          const uint32_t bf = mapa_shared(bar_kv_full(slot), 0);
+          const uint32_t dst = sKV + slot * kStage;
+          if (w == 0) {   // keys [64 r, 64 r + 64) of tile t, d in two 64-column boxes
+            for (int x = 0; x < 2; ++x)
+              tma_load_3d_pair(dst + x * HBOX, &tm_k, bf, x * 64, t * BN + 64 * (int)rank, g, HBOX);
+          } else {        // every key of tile t, d columns [64 r, 64 r + 64)
+            tma_load_3d_pair(dst, &tm_v, bf, 64 * (int)rank, t * BN, g, BOX);
+          }
+          if (++slot == STAGES) { slot = 0; phase ^= 1; }
+        }
+      }
+      // teardown: every slot's last release (a multicast commit from the leader) has landed in this
+      // CTA's barriers before the pair may exit
+      for (int s2 = 0; s2 < STAGES; ++s2) {
+        mbar_wait(bar_kv_empty(slot), phase ^ 1);
+        if (++slot == STAGES) { slot = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(2 * BM, BN, 0, 0);   // Q K-major, K K-major
+      constexpr uint32_t idesc_pv = make_idesc_bf16(2 * BM, D, 0, 1);   // P (TMEM), V MN-major
+      auto issue_s = [&](int b, int slot) {
+        const uint32_t qa = sQ + b * kQBytes, ka = sKV + slot * kStage;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ss_pair(tmem + b * BN, make_desc_sw128(qa + (kk / 4) * BOX + (kk % 4) * 32, 16, 1024),
+                      make_desc_sw128(ka + (kk / 4) * HBOX + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
+      };
+      auto issue_pv_half = [&](int b, int slot, int hf, bool acc) {   // keys [64 hf, 64 hf + 64)
+        const uint32_t va = sKV + slot * kStage;
+#pragma unroll
+        for (int k4 = 0; k4 < BN / 32; ++k4) {
+          const int kk = hf * (BN / 32) + k4;
+          mma_ts_pair(tmem + NH * BN + b * D, tmem + b * BN + kk * 8, make_desc_sw128(va + kk * 2048, BOX, 1024),
+                      idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      for (int b = 0; b < NH; ++b) mbar_wait_cluster(bar_q(b), 0);
+      int slot = 0;
+      uint32_t phase = 0;
+      mbar_wait_cluster(bar_kv_full(slot), phase);
+      tc_fence_after();
+      for (int b = 0; b < NH; ++b) { issue_s(b, slot); mma_commit_pair(bar_s_full(b)); }
+      mma_commit_pair(bar_kv_empty(slot));
+      if (++slot == STAGES) { slot = 0; phase ^= 1; }
+      for (int t = 0; t < nT; ++t) {
+        const int vslot = slot;
+        mbar_wait_cluster(bar_kv_full(vslot), phase);
+        if (++slot == STAGES) { slot = 0; phase ^= 1; }
+        const int kslot = slot;
+        const bool more = t + 1 < nT;
+        for (int b = 0; b < NH; ++b) {
+          mbar_wait_cluster(bar_p_half(b, 0), t & 1);
+          tc_fence_after();
+          issue_pv_half(b, vslot, 0, t > 0);
+          mbar_wait_cluster(bar_p_half(b, 1), t & 1);
+          tc_fence_after();
+          issue_pv_half(b, vslot, 1, true);
+          mma_commit_pair(bar_o_full(b));
+          if (more) {
+            if (b == 0) { mbar_wait_cluster(bar_kv_full(kslot), phase); tc_fence_after(); }
+            issue_s(b, kslot);
+            mma_commit_pair(bar_s_full(b));
+          }
+        }
+        mma_commit_pair(bar_kv_empty(vslot));
+        if (more) {
+          mma_commit_pair(bar_kv_empty(kslot));
+          if (++slot == STAGES) { slot = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax warpgroups (both CTAs)
+    const int b = (warp - 4) / 4;
+    const int wq = warp % 4;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + b * BN;
+    const uint32_t tO = tmem + lane_addr + NH * BN + b * D;
+    const float sl2 = a.scale_log2;
+    const f2_t sl2x2 = f2(sl2, sl2);
+    float m = -INFINITY, l = 0.f;
+    for (int t = 0; t < nT; ++t) {
+      mbar_wait(bar_s_full(b), t & 1);
+      tc_fence_after();
+      const bool diag = (t0 + t == T - 1);
+      uint32_t v[BN];
+#pragma unroll
+      for (int cc = 0; cc < BN / 32; ++cc) tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cc * 32));
+      tmem_wait_ld();
+      if (diag) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+          if (i > r) v[i] = __float_as_uint(-INFINITY);
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < BN; i += 4) {
+        mx0 = fmax3(mx0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+      }
+      const float m_new = fmaxf(m, fmaxf(mx0, mx1) * sl2);
+      const bool need = m_new > m + fwd::kRescaleThreshold;
+      const float m_use = need ? m_new : m;
+      const float alpha = need ? ex2(m - m_new) : 1.f;
+      l *= alpha;
+      // PV_b(t-1) is complete: S_b(t), issued after it by the same (leader) thread, has completed
+      if (t > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+        for (int cc = 0; cc < D / 8; ++cc) {
+          uint32_t ov[8];
+          tmem_ld8(tO + cc * 8, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st8(tO + cc * 8, ov);
+        }
+      }
+      m = m_use;
+      const f2_t negm = f2(-m_use, -m_use);
+      f2_t lsum0 = f2(0.f, 0.f), lsum1 = f2(0.f, 0.f);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const int cc = hf * 2 + c2;
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const f2_t x = ffma2(f2u(v[cc * 32 + i], v[cc * 32 + i + 1]), sl2x2, negm);
+            const f2_t p2 = f2(ex2(f2lo(x)), ex2(f2hi(x)));
+            if ((i / 2) & 1) lsum1 = fadd2(lsum1, p2); else lsum0 = fadd2(lsum0, p2);
+            pk[i / 2] = pack_bf16_f2(p2);
+          }
+          tmem_st16(tS + cc * 16, pk);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(bar_p_half(b, hf), 0));
+      }
+      const f2_t lsum = fadd2(lsum0, lsum1);
+      l += f2lo(lsum) + f2hi(lsum);
+    }
+    mbar_wait(bar_o_full(b), (nT - 1) & 1);
+    tc_fence_after();
+    const int h = h0 + b;
+    const float inv_l = 1.f / l;
+    const float lse_v = (m + __log2f(l)) * 0.69314718055994531f;
+    if (a.nsplit == 1) {
+      __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)(qt * BM + r) * a.qr;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        if (cc * 32 >= a.d_out) break;
+        uint32_t v[32];
+        tmem_ld32(tO + cc * 32, v);
+        tmem_wait_ld();
+        uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(v[8 * q + 0]) * inv_l, __uint_as_float(v[8 * q + 1]) * inv_l);
+          w.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l);
+          w.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l);
+          w.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l);
+          dst[q] = w;
+        }
+      }
+      SECO_CHECK_COND(h < a.hq && qt * BM + r < a.c, 522);
+      lse[(int64_t)h * a.c + qt * BM + r] = lse_v;
+    } else {
+      const int64_t prow = ((int64_t)split * a.hq + h) * a.c + qt * BM + r;
+      SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.c, 523);
+      float4* dst = reinterpret_cast<float4*>(a.part_o + prow * D);
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tO + cc * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          dst[cc * 8 + q] = make_float4(__uint_as_float(v[4 * q]) * inv_l, __uint_as_float(v[4 * q + 1]) * inv_l,
+                                        __uint_as_float(v[4 * q + 2]) * inv_l, __uint_as_float(v[4 * q + 3]) * inv_l);
+      }
+      a.part_lse[prow] = lse_v;
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                                    // neither CTA leaves while the pair still uses its smem / TMEM
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<512>(tmem);
+#if SECO_FWD_PDL
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 cudaError_t launch_fwd_combine(const ChunkGeom& g, int nsplit, const float* part_o, const float* part_lse, void* o,
                                float* lse, cudaStream_t st);
 
-template <int NH, int D, int STAGES>
+template <int NH, int D, int STAGES, bool PAIR>
 static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
                                    const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
                                    cudaStream_t st, int* launches) {
-  using L = fwd::Layout<NH, D, STAGES>;
+  using L = typename std::conditional<PAIR, fwd2::Layout<STAGES>, fwd::Layout<NH, D, STAGES>>::type;
   static_assert(L::kAlloc <= 232448, "shared memory budget");
-  auto kern = seco_fwd_sm100_kernel<NH, D, STAGES>;
+  static_assert(!PAIR || (NH == 2 && D == 128), "the pair kernel is NH = 2, D = 128");
+  auto kern = [] {
+    if constexpr (PAIR) return seco_fwd2_sm100_kernel<STAGES>;
+    else return seco_fwd_sm100_kernel<NH, D, STAGES>;
+  }();
   static std::atomic<unsigned long long> attr_done{0};
   {
     cudaError_t e = ensure_smem_attr(kern, L::kAlloc, attr_done);
@@ -470,6 +790,15 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   return e;
 }
 
+bool fwd_uses_pair(const ChunkGeom& g) {
+  static const bool enabled = [] {
+    // experiment, off by default (correct, -38 % per call); SECO_FWD_PAIR=1 selects it
+    const char* e = std::getenv("SECO_FWD_PAIR");
+    return e != nullptr && e[0] == '1';
+  }();
+  return enabled && (g.d == 128 || g.d == 64) && (g.hq / g.hkv) % 4 == 0;
+}
+
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
                              cudaStream_t st, int* launches) {
@@ -477,8 +806,11 @@ cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   // d = 64 runs the D = 128 kernel on zero-padded tiles: the tensor maps describe 64-column
   // rows, so the TMA fills the second 64-column box of every tile with zeros
   if (g.d == 128 || g.d == 64) {
-    if (G % 2 == 0) return launch_fwd_impl<2, 128, 5>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
-    return launch_fwd_impl<1, 128, 6>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
+    // groups of 4 q-heads per kv head (LLaMA): CTA pairs over the 4 heads of a group, K / V
+    // halves per CTA (tk must then have 64-row boxes: seco_api.cpp asks fwd_uses_pair)
+    if (fwd_uses_pair(g)) return launch_fwd_impl<2, 128, 8, true>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
+    if (G % 2 == 0) return launch_fwd_impl<2, 128, 5, false>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
+    return launch_fwd_impl<1, 128, 6, false>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
   }
   return cudaErrorInvalidValue;
 }

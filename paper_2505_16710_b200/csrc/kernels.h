@@ -40,6 +40,8 @@ cudaError_t launch_bwd_fp32(const ChunkGeom& g, const float* q, const float* k, 
                             cudaStream_t st, int* launches);
 
 // ---- bf16 tensor-core path (tcgen05 / TMEM / TMA) -----------------------------------
+// the forward runs as CTA pairs (tk must then be encoded with 64-row boxes, see seco_api.cpp)
+bool fwd_uses_pair(const ChunkGeom& g);
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
                              cudaStream_t st, int* launches);

@@ -12,6 +12,7 @@
 //          of those rows staged in smem); per-split partial sums of dA / dB to the workspace
 //   reduce partials added in split order into dA / dB
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -285,8 +286,18 @@ SECO_DEV void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uin
                : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// 16-B read-only load, zero when !ok.  asm volatile keeps the loads of a batch in program order
+// ahead of the (also volatile) MMAs that consume them: the compiler would otherwise sink each
+// load next to its first use and leave only a few of them in flight
 SECO_DEV uint4 ldg16(const __nv_bfloat16* p, bool ok) {
-  return ok ? __ldg(reinterpret_cast<const uint4*>(p)) : make_uint4(0u, 0u, 0u, 0u);
+  uint4 v;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+      "@q ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "r"((int)ok));
+  return v;
 }
 // bf16 hi / lo split of two fp32 values (lower k in the low half): x ~= hi + lo
 SECO_DEV void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
@@ -356,29 +367,40 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][nt][e] = 0.f;
-#pragma unroll 2
-  for (int ks = warp; ks < chunk / 32; ks += 4) {
-    const int cl = ks * 32;                         // column of the step within the chunk
-    uint4 xv[4][2];
+  // batches of BATCH k32 steps per warp: all X / dY loads of a batch are issued before its MMAs
+  // (16 x 16-B loads in flight per thread), steps past the chunk load zeros
+  constexpr int BATCH = 2;
+  for (int ks0 = warp; ks0 < nks; ks0 += 4 * BATCH) {
+    uint4 xv[BATCH][4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = row0 + 16 * i + g;
-      xv[i][0] = ldg16(M + (int64_t)r * ld + col_c + cl + 8 * q, r < p.rows);
-      xv[i][1] = ldg16(M + (int64_t)(r + 8) * ld + col_c + cl + 8 * q, r + 8 < p.rows);
+    for (int bb = 0; bb < BATCH; ++bb) {
+      const int ks = ks0 + 4 * bb;
+      const bool ok = ks < nks;
+      const int cl = ks * 32;                       // column of the step within the chunk
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = row0 + 16 * i + g;
+        xv[bb][i][0] = ldg16(M + (int64_t)r * ld + col_c + cl + 8 * q, ok && r < p.rows);
+        xv[bb][i][1] = ldg16(M + (int64_t)(r + 8) * ld + col_c + cl + 8 * q, ok && r + 8 < p.rows);
+      }
     }
-    uint32_t bf[NT][4];     // b0 / b1 of mma 0, b0 / b1 of mma 1
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const uint4 v = sfrag[(ks * NT + nt) * 32 + lane];
-      bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int bb = 0; bb < BATCH; ++bb) {
+      const int ks = ks0 + 4 * bb;
+      uint32_t bf[NT][4];   // b0 / b1 of mma 0, b0 / b1 of mma 1
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        mma16816(acc[i][nt], xv[i][0].x, xv[i][1].x, xv[i][0].y, xv[i][1].y, bf[nt][0], bf[nt][1]);
-        mma16816(acc[i][nt], xv[i][0].z, xv[i][1].z, xv[i][0].w, xv[i][1].w, bf[nt][2], bf[nt][3]);
+        const uint4 v = ks < nks ? sfrag[(ks * NT + nt) * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
+        bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma16816(acc[i][nt], xv[bb][i][0].x, xv[bb][i][1].x, xv[bb][i][0].y, xv[bb][i][1].y, bf[nt][0], bf[nt][1]);
+          mma16816(acc[i][nt], xv[bb][i][0].z, xv[bb][i][1].z, xv[bb][i][0].w, xv[bb][i][1].w, bf[nt][2], bf[nt][3]);
+        }
+    }
   }
   // warp partials -> smem, summed in warp order
 #pragma unroll
@@ -444,29 +466,40 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[j][nt][e] = 0.f;
-#pragma unroll 4
-  for (int s = s0; s < s1; ++s) {
-    const int r = 16 * s + 2 * q;
-    uint4 v[4];
-    v[0] = ldg16(M + (int64_t)r * ld + c0, r < p.rows);
-    v[1] = ldg16(M + (int64_t)(r + 1) * ld + c0, r + 1 < p.rows);
-    v[2] = ldg16(M + (int64_t)(r + 8) * ld + c0, r + 8 < p.rows);
-    v[3] = ldg16(M + (int64_t)(r + 9) * ld + c0, r + 9 < p.rows);
-    uint4 f[NT];
+  // batches of BATCH 16-row steps: all loads of a batch (4 x 16 B of X / dY rows and the
+  // fragment per step) are issued before its MMAs; steps past the split load zeros
+  constexpr int BATCH = NT == 1 ? 4 : 2;
+  for (int sb = s0; sb < s1; sb += BATCH) {
+    uint4 v[BATCH][4];
+    uint4 f[BATCH][NT];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) f[nt] = frag[((int64_t)s * NT + nt) * 32 + lane];
-    const uint32_t* w0 = &v[0].x;
-    const uint32_t* w1 = &v[1].x;
-    const uint32_t* w2 = &v[2].x;
-    const uint32_t* w3 = &v[3].x;
+    for (int bb = 0; bb < BATCH; ++bb) {
+      const int s = sb + bb;
+      const bool ok = s < s1;
+      const int r = 16 * s + 2 * q;
+      v[bb][0] = ldg16(M + (int64_t)r * ld + c0, ok && r < p.rows);
+      v[bb][1] = ldg16(M + (int64_t)(r + 1) * ld + c0, ok && r + 1 < p.rows);
+      v[bb][2] = ldg16(M + (int64_t)(r + 8) * ld + c0, ok && r + 8 < p.rows);
+      v[bb][3] = ldg16(M + (int64_t)(r + 9) * ld + c0, ok && r + 9 < p.rows);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t a0 = __byte_perm(w0[j], w1[j], 0x5410), a1 = __byte_perm(w0[j], w1[j], 0x7632);
-      const uint32_t a2 = __byte_perm(w2[j], w3[j], 0x5410), a3 = __byte_perm(w2[j], w3[j], 0x7632);
+      for (int nt = 0; nt < NT; ++nt)
+        f[bb][nt] = ok ? frag[((int64_t)s * NT + nt) * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
+    }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        mma16816(acc[j][nt], a0, a1, a2, a3, f[nt].x, f[nt].y);   // hi
-        mma16816(acc[j][nt], a0, a1, a2, a3, f[nt].z, f[nt].w);   // lo
+    for (int bb = 0; bb < BATCH; ++bb) {
+      const uint32_t* w0 = &v[bb][0].x;
+      const uint32_t* w1 = &v[bb][1].x;
+      const uint32_t* w2 = &v[bb][2].x;
+      const uint32_t* w3 = &v[bb][3].x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t a0 = __byte_perm(w0[j], w1[j], 0x5410), a1 = __byte_perm(w0[j], w1[j], 0x7632);
+        const uint32_t a2 = __byte_perm(w2[j], w3[j], 0x5410), a3 = __byte_perm(w2[j], w3[j], 0x7632);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma16816(acc[j][nt], a0, a1, a2, a3, f[bb][nt].x, f[bb][nt].y);   // hi
+          mma16816(acc[j][nt], a0, a1, a2, a3, f[bb][nt].z, f[bb][nt].w);   // lo
+        }
       }
     }
   }
@@ -501,7 +534,11 @@ size_t tu_smem(int n_in, int n_out) {
 }  // namespace lora_tc
 
 bool lora_tc_ok(const LoraGeom& g) {
-  return g.n_in % 256 == 0 && g.n_out % 256 == 0 && g.ldx % 8 == 0 && g.ldy % 8 == 0 &&
+  static const bool enabled = [] {
+    const char* e = std::getenv("SECO_LORA_TC");     // A/B switch: SECO_LORA_TC=0 selects the CUDA-core kernels
+    return e == nullptr || e[0] != '0';
+  }();
+  return enabled && g.n_in % 256 == 0 && g.n_out % 256 == 0 && g.ldx % 8 == 0 && g.ldy % 8 == 0 &&
          (g.rank == 1 || g.rank == 2 || g.rank == 4 || g.rank == 8 || g.rank == 16) &&
          lora_tc::tu_smem<16>(g.n_in, g.n_out) <= 200 * 1024;
 }

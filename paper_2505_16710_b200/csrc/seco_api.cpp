@@ -242,7 +242,8 @@ seco_status seco_chunk_forward(const seco_shape* s, int32_t j, const void* q, co
   const int S_used = (j + 1) * s->chunk;
   CUtensorMap tq, tk, tv;
   if (!encode_3d(&tq, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 128) ||
-      !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
+      !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride,
+                 seco::fwd_uses_pair(g) ? 64 : 128) ||   // CTA pairs load K in 64-key halves
       !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128))
     return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   if (ws && !aligned16(ws)) return fail(SECO_ERR_ARG, "ws must be 16-byte aligned");
