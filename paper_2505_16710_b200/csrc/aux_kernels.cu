@@ -154,28 +154,41 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
                                                         T* __restrict__ dv_own, FinalArgs a) {
   const int bid = blockIdx.x;
   const int dv4 = a.d / 4, ld4 = a.ldq / 4;
+  const int lane = threadIdx.x % 32;
   if (bid < a.nQ) {
     if (dqacc == nullptr) return;
-    const int64_t rows = (int64_t)a.hq * a.c;
-    for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < rows * dv4; i += (int64_t)a.nQ * blockDim.x) {
-      const int64_t row = i / dv4;
-      const int x = (int)(i - row * dv4) * 4;
-      const int64_t h = row / a.c, r = row - h * a.c;
-      float4 v = reinterpret_cast<const float4*>(dqacc)[row * ld4 + x / 4];
-      v.x *= a.dq_scale; v.y *= a.dq_scale; v.z *= a.dq_scale; v.w *= a.dq_scale;
-      Vec4<T>::store(dq + h * a.qh + r * a.qr + x, v);
+    // one warp per row (h, r) in a grid-stride loop, 4 rows in flight; lanes stride the row's
+    // float4s (no 64-bit index divisions in the loop)
+    const int rows = a.hq * a.c;
+    const int gw = bid * 8 + threadIdx.x / 32, nw = a.nQ * 8;
+    constexpr int B = 4;
+    for (int row0 = gw * B; row0 < rows; row0 += nw * B) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int row = row0 + u;
+        if (row >= rows) break;
+        const int h = row / a.c, r = row - h * a.c;
+        const float4* src = reinterpret_cast<const float4*>(dqacc) + (int64_t)row * ld4;
+        T* dst = dq + (int64_t)h * a.qh + (int64_t)r * a.qr;
+        for (int x4 = lane; x4 < dv4; x4 += 32) {
+          float4 v = src[x4];
+          v.x *= a.dq_scale; v.y *= a.dq_scale; v.z *= a.dq_scale; v.w *= a.dq_scale;
+          Vec4<T>::store(dst + 4 * x4, v);
+        }
+      }
     }
   } else {
     if (dk_own == nullptr && dv_own == nullptr) return;
-    const int64_t per4 = (int64_t)a.c * dv4;          // one slot of one head, in float4 units
-    const int64_t total = 2 * (int64_t)a.hkv * per4;
-    for (int64_t i = (int64_t)(bid - a.nQ) * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)a.nO * blockDim.x) {
-      const int64_t th = i / per4, off4 = i - th * per4;
-      const int t = (int)(th / a.hkv), g = (int)(th % a.hkv);
-      const float4 v = reinterpret_cast<const float4*>(dkv + th * (int64_t)a.S * a.d + (int64_t)a.j * a.c * a.d)[off4];
-      T* dst = t == 0 ? dk_own : dv_own;
-      if (dst) Vec4<T>::store(dst + (int64_t)g * a.c * a.d + off4 * 4, v);
+    // rows of slot j: (tensor, kv head, row) -> own copy [hkv][c][d]
+    const int rows = 2 * a.hkv * a.c;
+    const int gw = (bid - a.nQ) * 8 + threadIdx.x / 32, nw = a.nO * 8;
+    for (int row = gw; row < rows; row += nw) {
+      const int th = row / a.c, r = row - th * a.c;            // th = tensor * hkv + g
+      T* own = th < a.hkv ? dk_own : dv_own;
+      if (own == nullptr) continue;
+      const float4* src = reinterpret_cast<const float4*>(dkv + (int64_t)th * a.S * a.d + ((int64_t)a.j * a.c + r) * a.d);
+      T* dst = own + ((int64_t)(th % a.hkv) * a.c + r) * a.d;
+      for (int x4 = lane; x4 < dv4; x4 += 32) Vec4<T>::store(dst + 4 * x4, src[x4]);
     }
   }
 }
@@ -254,20 +267,22 @@ __global__ void __launch_bounds__(256) chunk_skip_kernel(float* __restrict__ dkv
   const int dv4 = a.d / 4;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   if (bid < a.nQ) {
+    // one warp per row (h, r), grid-stride; 16-B stores when the rows allow, else 4 elements
     constexpr int E = 16 / sizeof(T);          // elements per 16-B store
     const int per = a.vec ? E : 4;
-    const int dvp = a.d / per;
-    const int64_t total = (int64_t)a.hq * a.c * dvp;
-    for (int64_t i = (int64_t)bid * blockDim.x + threadIdx.x; i < total; i += (int64_t)a.nQ * blockDim.x) {
-      const int64_t row = i / dvp;
-      const int x = (int)(i - row * dvp) * per;
-      const int64_t h = row / a.c, r = row - h * a.c;
-      T* dst = dq + h * a.qh + r * a.qr + x;
-      if (a.vec) {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
-      } else {                                  // element stores: fp32 dq strides need no 16-B alignment
+    const int lane = threadIdx.x % 32;
+    const int rows = a.hq * a.c;
+    for (int row = bid * 8 + threadIdx.x / 32; row < rows; row += a.nQ * 8) {
+      const int h = row / a.c, r = row - h * a.c;
+      T* base = dq + (int64_t)h * a.qh + (int64_t)r * a.qr;
+      for (int x = lane * per; x < a.d; x += 32 * per) {
+        T* dst = base + x;
+        if (a.vec) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+        } else {                                // element stores: fp32 dq strides need no 16-B alignment
 #pragma unroll
-        for (int e = 0; e < 4; ++e) stf(dst + e, 0.f);
+          for (int e = 0; e < 4; ++e) stf(dst + e, 0.f);
+        }
       }
     }
   } else {

@@ -337,3 +337,51 @@ def test_bf16_forward_waits_for_producer_kernel():
         outs.append((layer.o.clone(), layer.lse.clone()))
     assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
     assert torch.equal(outs[0][1].view(torch.int32), outs[1][1].view(torch.int32))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_spaco_expectation_through_the_kernels(dtype):
+    """North-star check (b) on the GPU path: averaging the C-ABI SpaCO step over EVERY sampled set
+    with its probability reproduces the oracle's exact expectation (O7): unbiased
+    (= the SeCO gradient) under independent Bernoulli(rho) inclusion with s = gamma = 1/rho
+    (reading Z7), and the closed-form biased factors t/k, t(t-1)/(k(k-1)) under Alg. 2's
+    literal t-of-k sampling."""
+    import itertools
+    from oracle import expectation as OE
+    hq, hkv, seq = 4, 1, 512
+    d, c = (16, 128) if dtype == torch.float32 else (128, 128)
+    k = seq // c
+    x = inputs(hq, hkv, seq, d, seed=17, dtype=dtype)
+    q, kk, v, do = upload(x, dtype)
+    layer = _layer(hq, hkv, d, seq, c, dtype)
+    tol = FP32_TOL if dtype == torch.float32 else BF16_TOL
+    parts = OE.decompose(x.q, x.k, x.v, x.do, [c] * k)
+    # Bernoulli(1/2), s = gamma = 2: the weighted mean over all 2^k sets is the SeCO gradient
+    rho = 0.5
+    acc = {n: 0.0 for n in ("dq", "dk", "dv")}
+    for n in range(k + 1):
+        for sel in itertools.combinations(range(k), n):
+            layer.step(q, kk, v, do, list(sel), 1 / rho, 1 / rho)
+            w = rho ** n * (1 - rho) ** (k - n)
+            acc["dq"] = acc["dq"] + w * layer.dq.double()
+            acc["dk"] = acc["dk"] + w * layer.dkv[0].double()
+            acc["dv"] = acc["dv"] + w * layer.dkv[1].double()
+    torch.cuda.synchronize()
+    ref = OE.closed_form_bernoulli(parts, rho, 1 / rho, 1 / rho)
+    seco = OC.seco_step(x.q, x.k, x.v, x.do, [c] * k)
+    for n in ("dq", "dk", "dv"):
+        assert err(acc[n].cpu().numpy(), ref[n]) <= tol, ("bernoulli", n)
+        assert err(acc[n].cpu().numpy(), seco[n]) <= tol, ("bernoulli = seco", n)
+    # t-of-k (PAPER mode, no cap): uniform mean over the C(k, t) sets = the biased closed form
+    t, gamma = 2, k / 2
+    acc = {n: 0.0 for n in ("dq", "dk", "dv")}
+    sets = list(itertools.combinations(range(k), t))
+    for sel in sets:
+        layer.step(q, kk, v, do, list(sel), gamma, 1.0)
+        acc["dq"] = acc["dq"] + layer.dq.double() / len(sets)
+        acc["dk"] = acc["dk"] + layer.dkv[0].double() / len(sets)
+        acc["dv"] = acc["dv"] + layer.dkv[1].double() / len(sets)
+    torch.cuda.synchronize()
+    ref = OE.closed_form_t_of_k(parts, k, t, gamma, 1.0)
+    for n in ("dq", "dk", "dv"):
+        assert err(acc[n].cpu().numpy(), ref[n]) <= tol, ("t-of-k", n)
