@@ -205,7 +205,7 @@ static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, flo
   a.nZ = dqacc ? 296 : 0;
   a.order = order;
   a.ldq = g.ldq ? g.ldq : g.d;
-  a.n_order = g.hq * ((g.c + 127) / 128);
+  a.n_order = g.hq * ((g.c + 127) / 128) + 1;   // order counters + the deterministic-mode work ticket
   bwd_prep_kernel<T><<<a.nD + a.nR + a.nZ, 256, 0, st>>>(o, d_o, D, dkv, dqacc, lse, nlse, a);
   return cudaGetLastError();
 }

@@ -104,6 +104,7 @@ struct Args {
   float* dqacc;       // [hq][c][D] fp32 dQ accumulator (zeroed by bwd_prep)
   int* dq_order;      // deterministic mode: [hq][c/BQ] count of key tiles that have added their
                       // dQ share of query tile (h, qt) (zeroed by bwd_prep); null otherwise
+  int* ticket;        // deterministic mode: work-unit ticket counter (zeroed by bwd_prep); null otherwise
   int* err;           // set to 1 if the dynamic smem window is not 1024-B aligned
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters] clock64
 };
@@ -157,8 +158,17 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
 #define TRACE(slot, i) do { } while (0)
 #endif
   // block -> (unit U, piece of f); units in ascending key-tile order = longest work first,
-  // the split (shorter) pieces at the end of the list fill the last wave
-  const int bid = blockIdx.x;
+  // the split (shorter) pieces at the end of the list fill the last wave.  Deterministic mode
+  // takes its work item from a ticket drawn when the CTA starts: a unit's dQ adds wait only for
+  // lower units, which were claimed by CTAs already running, so progress does not depend on
+  // the order in which the hardware dispatches blocks.
+  __shared__ int s_ticket;
+  int bid = blockIdx.x;
+  if (a.ticket) {
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    bid = s_ticket;
+  }
   int U, piece, f;
   if (bid < a.n0) {
     U = bid; piece = 0; f = 1;
@@ -1096,6 +1106,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   a.dk_scale = gscale * g.scale;
   a.dv_scale = gscale;
   a.nlse = ws_D + (size_t)g.hq * g.c; a.Dv = ws_D; a.dqacc = ws_dqacc; a.dq_order = order;
+  a.ticket = order ? order + (size_t)g.hq * (g.c / bwd::BQ) : nullptr;   // zeroed with the counters
   a.err = nullptr;
   a.trace = nullptr;
 #ifdef SECO_TRACE
