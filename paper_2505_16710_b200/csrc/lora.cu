@@ -317,7 +317,33 @@ struct Args {
   uint4* frag;              // [2 (0: t, 1: u)][nsteps][NT][32] hi/lo B fragments
 };
 
+// ---------------------------------------------------------------- shared-memory staging
+// cp.async (16 B, L2 -> smem, zero-filled when !ok): each warp copies whole row segments, so
+// every load instruction reads contiguous 512 B of a row (HBM-friendly), and a CTA has its
+// whole tile in flight at once without spending registers on it
+SECO_DEV void cp_async16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+SECO_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+SECO_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+SECO_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+SECO_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
 // ---------------------------------------------------------------- pass 1: t = X A, u = dY B^T
+// CTA (chunk c of the cluster, 64-row block, tensor): the [64 rows][n / 8 columns] tile goes to
+// smem in one burst of cp.async (rows padded by 16 B: conflict-free ldmatrix); warp w then owns
+// rows [16 w, 16 w + 16) and walks the chunk in k16 steps (ldmatrix A fragment, B fragments of
+// the A / B slice staged in mma order).  The 8 chunk partials of a row block are summed in
+// rank order through DSMEM.
 template <int R>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
     lora_tu_kernel(const Args p) {
@@ -332,88 +358,70 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
   const int row0 = blockIdx.y * kRowsTU;
   const __nv_bfloat16* M = tau ? p.dy : p.x;
   const int64_t ld = tau ? p.ldy : p.ldx;
-  // smem: B fragments of the chunk in mma order [k32 step][NT][lane] (16 B each: b0 / b1 of the
-  // step's two mmas) | warp partials [4][64][RP] | CTA partial [64][RP] | one step [16][RP]
-  const int nks = chunk / 32;
-  uint4* sfrag = reinterpret_cast<uint4*>(smem_raw);
-  float* red = reinterpret_cast<float*>(smem_raw + (size_t)nks * NT * 32 * 16);
-  float* part = red + 4 * kRowsTU * RP;
+  const int rstride = chunk * 2 + 16;               // bytes per staged row
+  const int nk16 = chunk / 16;
+  // smem: X / dY tile [64][chunk] | B fragments [k16 step][NT][lane] (uint2) | CTA partial [64][RP]
+  //       | one 16-row step [16][RP]
+  uint8_t* sx = smem_raw;
+  uint2* sfrag = reinterpret_cast<uint2*>(smem_raw + kRowsTU * rstride);
+  float* part = reinterpret_cast<float*>(sfrag + nk16 * NT * 32);
   float* stepv = part + kRowsTU * RP;
-  // lane (g, q) of step ks, n-tile nt needs the operand at k = 8q..8q+7 of the step, n = 8 nt + g
-  for (int e = threadIdx.x; e < nks * NT * 32; e += kThreads) {
-    const int ln = e % 32, nt = (e / 32) % NT, ks = e / (32 * NT);
-    const int nn = 8 * nt + ln / 4, k0 = col_c + 32 * ks + 8 * (ln % 4);
-    uint4 f = make_uint4(0u, 0u, 0u, 0u);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q = lane % 4;
+  {
+    const uint32_t sxa = smem_u32(sx);
+    const int vpr = chunk / 8;                      // 16-B vectors per row
+    for (int e = threadIdx.x; e < kRowsTU * vpr; e += kThreads) {
+      const int r = e / vpr, v = e % vpr;
+      const bool ok = row0 + r < p.rows;
+      cp_async16(sxa + r * rstride + v * 16, M + (int64_t)(ok ? row0 + r : 0) * ld + col_c + v * 8, ok);
+    }
+    cp_async_commit();
+  }
+  // B fragments, standard k order: lane (g, q) of step s needs k = 16 s + {2q, 2q+1} (b0) and
+  // {2q+8, 2q+9} (b1) at n = 8 nt + g
+  for (int e = threadIdx.x; e < nk16 * NT * 32; e += kThreads) {
+    const int ln = e % 32, nt = (e / 32) % NT, s = e / (32 * NT);
+    const int nn = 8 * nt + ln / 4, k0 = col_c + 16 * s + 2 * (ln % 4);
+    uint2 f = make_uint2(0u, 0u);
     if (nn < R) {
-      if (tau == 0) {   // A [n_in][R]: column nn over 8 consecutive rows, packed in k pairs
-        uint32_t w[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          w[t] = (uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 2 * t) * R + nn]) |
-                 ((uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 2 * t + 1) * R + nn]) << 16);
-        f = make_uint4(w[0], w[1], w[2], w[3]);
-      } else {          // B [R][n_out]: row nn, 8 consecutive columns
-        f = __ldg(reinterpret_cast<const uint4*>(p.b + (int64_t)nn * p.n_out + k0));
+      if (tau == 0) {   // A [n_in][R]
+        f.x = (uint32_t)__bfloat16_as_ushort(p.a[(int64_t)k0 * R + nn]) |
+              ((uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 1) * R + nn]) << 16);
+        f.y = (uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 8) * R + nn]) |
+              ((uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 9) * R + nn]) << 16);
+      } else {          // B [R][n_out]
+        const __nv_bfloat16* br = p.b + (int64_t)nn * p.n_out + k0;
+        f.x = *reinterpret_cast<const uint32_t*>(br);
+        f.y = *reinterpret_cast<const uint32_t*>(br + 8);
       }
     }
     sfrag[e] = f;
   }
+  cp_async_wait<0>();
   __syncthreads();
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q = lane % 4;
-  float acc[4][NT][4];
+  float acc[NT][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[i][nt][e] = 0.f;
-  // batches of BATCH k32 steps per warp: all X / dY loads of a batch are issued before its MMAs
-  // (16 x 16-B loads in flight per thread), steps past the chunk load zeros
-  constexpr int BATCH = 2;
-  for (int ks0 = warp; ks0 < nks; ks0 += 4 * BATCH) {
-    uint4 xv[BATCH][4][2];
-#pragma unroll
-    for (int bb = 0; bb < BATCH; ++bb) {
-      const int ks = ks0 + 4 * bb;
-      const bool ok = ks < nks;
-      const int cl = ks * 32;                       // column of the step within the chunk
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = row0 + 16 * i + g;
-        xv[bb][i][0] = ldg16(M + (int64_t)r * ld + col_c + cl + 8 * q, ok && r < p.rows);
-        xv[bb][i][1] = ldg16(M + (int64_t)(r + 8) * ld + col_c + cl + 8 * q, ok && r + 8 < p.rows);
-      }
-    }
-#pragma unroll
-    for (int bb = 0; bb < BATCH; ++bb) {
-      const int ks = ks0 + 4 * bb;
-      uint32_t bf[NT][4];   // b0 / b1 of mma 0, b0 / b1 of mma 1
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const uint4 v = ks < nks ? sfrag[(ks * NT + nt) * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
-        bf[nt][0] = v.x; bf[nt][1] = v.y; bf[nt][2] = v.z; bf[nt][3] = v.w;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          mma16816(acc[i][nt], xv[bb][i][0].x, xv[bb][i][1].x, xv[bb][i][0].y, xv[bb][i][1].y, bf[nt][0], bf[nt][1]);
-          mma16816(acc[i][nt], xv[bb][i][0].z, xv[bb][i][1].z, xv[bb][i][0].w, xv[bb][i][1].w, bf[nt][2], bf[nt][3]);
-        }
-    }
-  }
-  // warp partials -> smem, summed in warp order
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+  // ldmatrix row address of this lane: rows 16 w + (lane % 16), k offset 8 (lane / 16)
+  const uint32_t arow = smem_u32(sx) + (16 * warp + lane % 16) * rstride + (lane / 16) * 16;
+#pragma unroll 4
+  for (int s = 0; s < nk16; ++s) {
+    uint32_t a0, a1, a2, a3;
+    ldsm_x4(arow + s * 32, a0, a1, a2, a3);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      float* w0 = red + (warp * kRowsTU + 16 * i + g) * RP + 8 * nt + 2 * q;
-      w0[0] = acc[i][nt][0]; w0[1] = acc[i][nt][1];
-      w0[8 * RP] = acc[i][nt][2]; w0[8 * RP + 1] = acc[i][nt][3];
+      const uint2 f = sfrag[(s * NT + nt) * 32 + lane];
+      mma16816(acc[nt], a0, a1, a2, a3, f.x, f.y);
     }
-  __syncthreads();
-  for (int e = threadIdx.x; e < kRowsTU * RP; e += kThreads)
-    part[e] = red[e] + red[kRowsTU * RP + e] + red[2 * kRowsTU * RP + e] + red[3 * kRowsTU * RP + e];
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    float* w0 = part + (16 * warp + g) * RP + 8 * nt + 2 * q;
+    w0[0] = acc[nt][0]; w0[1] = acc[nt][1];
+    w0[8 * RP] = acc[nt][2]; w0[8 * RP + 1] = acc[nt][3];
+  }
   cluster.sync();                                   // every chunk's partial is visible
   const int rank = (int)cluster.block_rank();
   if (rank < kRowsTU / 16) {                        // ranks 0..3: one 16-row step each
@@ -442,13 +450,22 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- pass 2: dA += X^T u, dB += t^T dY
+// CTA (row split r of the cluster, 256-column group of [X | dY]): 64-row slabs of the group go
+// to smem through a 3-deep cp.async ring; warp w owns columns [64 w, 64 w + 64) (4 m16 tiles:
+// columns are M, rows are K) and takes its A fragments with ldmatrix.trans; the B fragments are
+// pass 1's hi / lo fragments of u (for X) or t (for dY).  The 8 row-split partials are summed in
+// rank order through DSMEM and added into dA / dB.
 template <int R>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
     lora_grad_kernel(const Args p) {
   constexpr int NT = (R + 7) / 8, RP = 8 * NT;
+  constexpr int SLAB = 64, NSTAGE = 3;
+  constexpr int RS = kColsG * 2 + 16;               // bytes per staged row
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  __shared__ float part[kColsG * RP];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  float* part = reinterpret_cast<float*>(smem_raw);                    // [256 columns][RP]
+  uint8_t* ring = smem_raw + kColsG * RP * 4;                          // [NSTAGE][SLAB][RS]
   const int rank = (int)cluster.block_rank();
   const int gcol = blockIdx.y * kColsG;             // global column of [X | dY]
   const bool isA = gcol < p.n_in;
@@ -457,8 +474,20 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
   const int col0 = isA ? gcol : gcol - p.n_in;
   const uint4* frag = p.frag + (int64_t)(isA ? 1 : 0) * p.nsteps * NT * 32;   // X^T u, t^T dY
   const int s0 = rank * p.nsteps / kCluster, s1 = (rank + 1) * p.nsteps / kCluster;
+  const int r_begin = 16 * s0, r_end = 16 * s1;     // this split's rows (padded to 16)
+  const int nslab = (r_end - r_begin + SLAB - 1) / SLAB;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q = lane % 4;
-  const int c0 = col0 + 64 * warp + 8 * g;          // this thread's 8 columns
+  const uint32_t ring_a = smem_u32(ring);
+  auto load_slab = [&](int sl) {
+    const uint32_t base = ring_a + (sl % NSTAGE) * SLAB * RS;
+    for (int e = threadIdx.x; e < SLAB * (kColsG / 8); e += kThreads) {
+      const int r = e / (kColsG / 8), v = e % (kColsG / 8);
+      const int row = r_begin + sl * SLAB + r;
+      const bool ok = row < r_end && row < p.rows;
+      cp_async16(base + r * RS + v * 16, M + (int64_t)(ok ? row : 0) * ld + col0 + v * 8, ok);
+    }
+    cp_async_commit();
+  };
   float acc[4][NT][4];
 #pragma unroll
   for (int j = 0; j < 4; ++j)
@@ -466,51 +495,47 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[j][nt][e] = 0.f;
-  // batches of BATCH 16-row steps: all loads of a batch (4 x 16 B of X / dY rows and the
-  // fragment per step) are issued before its MMAs; steps past the split load zeros
-  constexpr int BATCH = NT == 1 ? 4 : 2;
-  for (int sb = s0; sb < s1; sb += BATCH) {
-    uint4 v[BATCH][4];
-    uint4 f[BATCH][NT];
+  for (int sl = 0; sl < NSTAGE - 1; ++sl) {
+    if (sl < nslab) load_slab(sl); else cp_async_commit();
+  }
+  // ldmatrix.trans: matrix i = lane / 8 covers stored rows (K) 8 (i / 2) .. +7 of the k16 step at
+  // stored columns (M) 16 j + 8 (i % 2); lane supplies row lane % 8 of it
+  const int li = lane / 8, lr = lane % 8;
+  const uint32_t lane_off = (uint32_t)((8 * (li / 2) + lr) * RS + (64 * warp + 8 * (li % 2)) * 2);
+  for (int sl = 0; sl < nslab; ++sl) {
+    if (sl + NSTAGE - 1 < nslab) load_slab(sl + NSTAGE - 1); else cp_async_commit();
+    cp_async_wait<NSTAGE - 1>();
+    __syncthreads();
+    const uint32_t base = ring_a + (sl % NSTAGE) * SLAB * RS + lane_off;
 #pragma unroll
-    for (int bb = 0; bb < BATCH; ++bb) {
-      const int s = sb + bb;
-      const bool ok = s < s1;
-      const int r = 16 * s + 2 * q;
-      v[bb][0] = ldg16(M + (int64_t)r * ld + c0, ok && r < p.rows);
-      v[bb][1] = ldg16(M + (int64_t)(r + 1) * ld + c0, ok && r + 1 < p.rows);
-      v[bb][2] = ldg16(M + (int64_t)(r + 8) * ld + c0, ok && r + 8 < p.rows);
-      v[bb][3] = ldg16(M + (int64_t)(r + 9) * ld + c0, ok && r + 9 < p.rows);
+    for (int kk = 0; kk < SLAB / 16; ++kk) {
+      const int s = (r_begin + sl * SLAB) / 16 + kk;   // global 16-row step
+      if (s >= s1) break;
+      uint4 f[NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        f[bb][nt] = ok ? frag[((int64_t)s * NT + nt) * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int bb = 0; bb < BATCH; ++bb) {
-      const uint32_t* w0 = &v[bb][0].x;
-      const uint32_t* w1 = &v[bb][1].x;
-      const uint32_t* w2 = &v[bb][2].x;
-      const uint32_t* w3 = &v[bb][3].x;
+      for (int nt = 0; nt < NT; ++nt) f[nt] = frag[((int64_t)s * NT + nt) * 32 + lane];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t a0 = __byte_perm(w0[j], w1[j], 0x5410), a1 = __byte_perm(w0[j], w1[j], 0x7632);
-        const uint32_t a2 = __byte_perm(w2[j], w3[j], 0x5410), a3 = __byte_perm(w2[j], w3[j], 0x7632);
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(base + kk * 16 * RS + j * 32, a0, a1, a2, a3);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          mma16816(acc[j][nt], a0, a1, a2, a3, f[bb][nt].x, f[bb][nt].y);   // hi
-          mma16816(acc[j][nt], a0, a1, a2, a3, f[bb][nt].z, f[bb][nt].w);   // lo
+          mma16816(acc[j][nt], a0, a1, a2, a3, f[nt].x, f[nt].y);   // hi
+          mma16816(acc[j][nt], a0, a1, a2, a3, f[nt].z, f[nt].w);   // lo
         }
       }
     }
+    __syncthreads();                                // the slab's stage may be refilled next
   }
-  // CTA partial [256 columns][RP]: tile j, m = g -> column 8g + 2j, m = g + 8 -> 8g + 2j + 1
+  cp_async_wait<0>();
+  // CTA partial [256 columns][RP]: tile j of warp w covers columns 64 w + 16 j + {g, g + 8}
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      float* d0 = part + (64 * warp + 8 * g + 2 * j) * RP + 8 * nt + 2 * q;
+      float* d0 = part + (64 * warp + 16 * j + g) * RP + 8 * nt + 2 * q;
       d0[0] = acc[j][nt][0]; d0[1] = acc[j][nt][1];
-      d0[RP] = acc[j][nt][2]; d0[RP + 1] = acc[j][nt][3];
+      d0[8 * RP] = acc[j][nt][2]; d0[8 * RP + 1] = acc[j][nt][3];
     }
   cluster.sync();
   // rank r adds columns [32 r, 32 r + 32) of the 8 row-split partials, in rank order
@@ -528,8 +553,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
 template <int R>
 size_t tu_smem(int n_in, int n_out) {
   constexpr int NT = (R + 7) / 8, RP = 8 * NT;
-  const int nmax = n_in > n_out ? n_in : n_out;
-  return (size_t)(nmax / kCluster / 32) * NT * 32 * 16 + (size_t)(4 * kRowsTU + kRowsTU + 16) * RP * 4;
+  const int chunk = (n_in > n_out ? n_in : n_out) / kCluster;
+  return (size_t)kRowsTU * (chunk * 2 + 16) + (size_t)(chunk / 16) * NT * 32 * 8 + (size_t)(kRowsTU + 16) * RP * 4;
+}
+template <int R>
+constexpr size_t grad_smem() {
+  return (size_t)kColsG * 8 * ((R + 7) / 8) * 4 + (size_t)3 * 64 * (kColsG * 2 + 16);
 }
 }  // namespace lora_tc
 
@@ -565,8 +594,11 @@ static cudaError_t launch_lora_tc(const LoraGeom& g, const void* x, const void* 
   dim3 g1(lora_tc::kCluster, (g.rows + lora_tc::kRowsTU - 1) / lora_tc::kRowsTU, 2);
   lora_tc::lora_tu_kernel<R><<<g1, lora_tc::kThreads, smem, st>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  static std::atomic<unsigned long long> attr_done2{0};
+  if ((e = ensure_smem_attr(lora_tc::lora_grad_kernel<R>, (int)lora_tc::grad_smem<R>(), attr_done2)) != cudaSuccess)
+    return e;
   dim3 g2(lora_tc::kCluster, (g.n_in + g.n_out) / lora_tc::kColsG);
-  lora_tc::lora_grad_kernel<R><<<g2, lora_tc::kThreads, 0, st>>>(p);
+  lora_tc::lora_grad_kernel<R><<<g2, lora_tc::kThreads, lora_tc::grad_smem<R>(), st>>>(p);
   return cudaGetLastError();
 }
 
