@@ -162,12 +162,12 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   // takes its work item from a ticket drawn when the CTA starts: a unit's dQ adds wait only for
   // lower units, which were claimed by CTAs already running, so progress does not depend on
   // the order in which the hardware dispatches blocks.
-  __shared__ int s_ticket;
   int bid = blockIdx.x;
-  if (a.ticket) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1);
+  if (a.ticket) {    // broadcast through the dynamic window (static smem would not fit beside it)
+    volatile int* s_ticket = reinterpret_cast<volatile int*>(smem + kTmemSlot + 8);
+    if (threadIdx.x == 0) *s_ticket = atomicAdd(a.ticket, 1);
     __syncthreads();
-    bid = s_ticket;
+    bid = *s_ticket;
   }
   int U, piece, f;
   if (bid < a.n0) {

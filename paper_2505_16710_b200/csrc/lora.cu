@@ -361,12 +361,32 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
   const int rstride = chunk * 2 + 16;               // bytes per staged row
   const int nk16 = chunk / 16;
   // smem: X / dY tile [64][chunk] | B fragments [k16 step][NT][lane] (uint2) | CTA partial [64][RP]
-  //       | one 16-row step [16][RP]
+  //       | one 16-row step [16][RP] | raw A / B slice of the chunk
   uint8_t* sx = smem_raw;
   uint2* sfrag = reinterpret_cast<uint2*>(smem_raw + kRowsTU * rstride);
   float* part = reinterpret_cast<float*>(sfrag + nk16 * NT * 32);
   float* stepv = part + kRowsTU * RP;
+  __nv_bfloat16* sraw = reinterpret_cast<__nv_bfloat16*>(stepv + 16 * RP);   // raw A / B slice
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q = lane % 4;
+  // group 0: the chunk's slice of A ([chunk][R], contiguous) or B ([R][chunk] rows of n_out)
+  if constexpr (R % 8 == 0) {
+    const uint32_t sr = smem_u32(sraw);
+    if (tau == 0) {
+      for (int e = threadIdx.x; e < chunk * R / 8; e += kThreads)
+        cp_async16(sr + e * 16, p.a + (int64_t)col_c * R + e * 8, true);
+    } else {
+      const int vpr = chunk / 8;
+      for (int e = threadIdx.x; e < R * vpr; e += kThreads) {
+        const int k = e / vpr, v = e % vpr;
+        cp_async16(sr + (k * chunk + v * 8) * 2, p.b + (int64_t)k * p.n_out + col_c + v * 8, true);
+      }
+    }
+  } else {
+    for (int e = threadIdx.x; e < chunk * R; e += kThreads)
+      sraw[e] = tau == 0 ? p.a[(int64_t)col_c * R + e] : p.b[(int64_t)(e / chunk) * p.n_out + col_c + e % chunk];
+  }
+  cp_async_commit();
+  // group 1: the [64 rows][chunk] X / dY tile, whole row segments per warp instruction
   {
     const uint32_t sxa = smem_u32(sx);
     const int vpr = chunk / 8;                      // 16-B vectors per row
@@ -377,22 +397,23 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
     }
     cp_async_commit();
   }
-  // B fragments, standard k order: lane (g, q) of step s needs k = 16 s + {2q, 2q+1} (b0) and
-  // {2q+8, 2q+9} (b1) at n = 8 nt + g
+  cp_async_wait<1>();                               // the slice has landed; the tile streams on
+  __syncthreads();
+  // B fragments in mma order, standard k order: lane (g, q) of step s needs k = 16 s + {2q, 2q+1}
+  // (b0) and {2q+8, 2q+9} (b1) at n = 8 nt + g
   for (int e = threadIdx.x; e < nk16 * NT * 32; e += kThreads) {
     const int ln = e % 32, nt = (e / 32) % NT, s = e / (32 * NT);
-    const int nn = 8 * nt + ln / 4, k0 = col_c + 16 * s + 2 * (ln % 4);
+    const int nn = 8 * nt + ln / 4, k0 = 16 * s + 2 * (ln % 4);
     uint2 f = make_uint2(0u, 0u);
     if (nn < R) {
-      if (tau == 0) {   // A [n_in][R]
-        f.x = (uint32_t)__bfloat16_as_ushort(p.a[(int64_t)k0 * R + nn]) |
-              ((uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 1) * R + nn]) << 16);
-        f.y = (uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 8) * R + nn]) |
-              ((uint32_t)__bfloat16_as_ushort(p.a[(int64_t)(k0 + 9) * R + nn]) << 16);
-      } else {          // B [R][n_out]
-        const __nv_bfloat16* br = p.b + (int64_t)nn * p.n_out + k0;
-        f.x = *reinterpret_cast<const uint32_t*>(br);
-        f.y = *reinterpret_cast<const uint32_t*>(br + 8);
+      if (tau == 0) {   // A slice [chunk][R]
+        f.x = (uint32_t)__bfloat16_as_ushort(sraw[k0 * R + nn]) |
+              ((uint32_t)__bfloat16_as_ushort(sraw[(k0 + 1) * R + nn]) << 16);
+        f.y = (uint32_t)__bfloat16_as_ushort(sraw[(k0 + 8) * R + nn]) |
+              ((uint32_t)__bfloat16_as_ushort(sraw[(k0 + 9) * R + nn]) << 16);
+      } else {          // B slice [R][chunk]
+        f.x = *reinterpret_cast<const uint32_t*>(sraw + nn * chunk + k0);
+        f.y = *reinterpret_cast<const uint32_t*>(sraw + nn * chunk + k0 + 8);
       }
     }
     sfrag[e] = f;
@@ -466,6 +487,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   float* part = reinterpret_cast<float*>(smem_raw);                    // [256 columns][RP]
   uint8_t* ring = smem_raw + kColsG * RP * 4;                          // [NSTAGE][SLAB][RS]
+  // the slab's hi / lo B fragments ride in the same ring stage: [NSTAGE][SLAB / 16][NT][32] uint4
+  uint8_t* fring = ring + NSTAGE * SLAB * RS;
   const int rank = (int)cluster.block_rank();
   const int gcol = blockIdx.y * kColsG;             // global column of [X | dY]
   const bool isA = gcol < p.n_in;
@@ -485,6 +508,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
       const int row = r_begin + sl * SLAB + r;
       const bool ok = row < r_end && row < p.rows;
       cp_async16(base + r * RS + v * 16, M + (int64_t)(ok ? row : 0) * ld + col0 + v * 8, ok);
+    }
+    const uint32_t fb = smem_u32(fring) + (sl % NSTAGE) * (SLAB / 16) * NT * 32 * 16;
+    const int sfirst = (r_begin + sl * SLAB) / 16;
+    for (int e = threadIdx.x; e < (SLAB / 16) * NT * 32; e += kThreads) {
+      const int st = sfirst + e / (NT * 32);
+      cp_async16(fb + e * 16, frag + (int64_t)(st < s1 ? st : s0) * NT * 32 + e % (NT * 32), st < s1);
     }
     cp_async_commit();
   };
@@ -512,8 +541,9 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads)
       const int s = (r_begin + sl * SLAB) / 16 + kk;   // global 16-row step
       if (s >= s1) break;
       uint4 f[NT];
+      const uint4* sf = reinterpret_cast<const uint4*>(fring) + ((sl % NSTAGE) * (SLAB / 16) + kk) * NT * 32;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) f[nt] = frag[((int64_t)s * NT + nt) * 32 + lane];
+      for (int nt = 0; nt < NT; ++nt) f[nt] = sf[nt * 32 + lane];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t a0, a1, a2, a3;
@@ -554,11 +584,13 @@ template <int R>
 size_t tu_smem(int n_in, int n_out) {
   constexpr int NT = (R + 7) / 8, RP = 8 * NT;
   const int chunk = (n_in > n_out ? n_in : n_out) / kCluster;
-  return (size_t)kRowsTU * (chunk * 2 + 16) + (size_t)(chunk / 16) * NT * 32 * 8 + (size_t)(kRowsTU + 16) * RP * 4;
+  return (size_t)kRowsTU * (chunk * 2 + 16) + (size_t)(chunk / 16) * NT * 32 * 8 + (size_t)(kRowsTU + 16) * RP * 4 +
+         (size_t)chunk * R * 2;
 }
 template <int R>
 constexpr size_t grad_smem() {
-  return (size_t)kColsG * 8 * ((R + 7) / 8) * 4 + (size_t)3 * 64 * (kColsG * 2 + 16);
+  return (size_t)kColsG * 8 * ((R + 7) / 8) * 4 + (size_t)3 * 64 * (kColsG * 2 + 16) +
+         (size_t)3 * 4 * ((R + 7) / 8) * 32 * 16;
 }
 }  // namespace lora_tc
 
