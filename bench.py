@@ -539,6 +539,57 @@ def main():
             if err != cudart.cudaError_t.cudaSuccess:
                 raise RuntimeError(f"cudaMemcpy2DAsync: {err}")
 
+        def e2e_steps(n_steps, step0):
+            """Enqueue n_steps pipelined end-to-end steps; returns the D2H-drained event of each."""
+            ends = []
+            for st_i in range(step0, step0 + n_steps):
+                b = st_i % 2
+                qd, kd, vd, dod = sets[b]
+                lay = layers[b]
+                ev_qkv, ev_do = [torch.cuda.Event() for _ in range(k)], [torch.cuda.Event() for _ in range(k)]
+                with torch.cuda.stream(s_in):
+                    if done[b] is not None:
+                        s_in.wait_event(done[b])
+                    for j in range(k):                       # stage-1 order
+                        for dst, src in ((kd, host[1]), (vd, host[2]), (qd, host[0])):
+                            rows(dst, j).copy_(rows(src, j), non_blocking=True)
+                        ev_qkv[j].record(s_in)
+                    for j in reversed(range(k)):             # stage-2 order
+                        rows(dod, j).copy_(rows(host[3], j), non_blocking=True)
+                        ev_do[j].record(s_in)
+                if drained[b] is not None:
+                    stream.wait_event(drained[b])
+                qv, kv, vv, dov = (t.transpose(0, 1) for t in (qd, kd, vd, dod))
+                lay.dkv.zero_()
+                ev_out = {}
+                for n_op, op in enumerate(order):
+                    j = op[1]
+                    if op[0] == "f":
+                        if n_op < k:                         # stage 1: chunk j's K, V, Q have arrived
+                            stream.wait_event(ev_qkv[j])
+                        lay.forward_chunk(qv, kv, vv, j, chained=op[2])
+                    elif op[0] == "b":
+                        stream.wait_event(ev_do[j])
+                        lay.backward_chunk(qv, kv, vv, dov, j, gamma, sscale)
+                    else:
+                        lay.skip_chunk(j)
+                    if op[0] in "bz":
+                        ev_out[j] = torch.cuda.Event()
+                        ev_out[j].record(stream)
+                done[b] = torch.cuda.Event()
+                done[b].record(stream)
+                with torch.cuda.stream(s_out):
+                    for j in stage2:
+                        s_out.wait_event(ev_out[j])
+                        d2h_chunk(b, j)
+                    drained[b] = torch.cuda.Event(enable_timing=True)
+                    drained[b].record(s_out)
+                ends.append(drained[b])
+            return ends
+
+        # untimed warm-up steps of the same pipeline (first-call costs of the copy paths)
+        e2e_steps(max(args.warmup, 1), 0)
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
@@ -546,60 +597,24 @@ def main():
         e0.record(s_in)
         stream.wait_event(e0)
         s_out.wait_event(e0)
-        for st_i in range(args.steps):
-            b = st_i % 2
-            qd, kd, vd, dod = sets[b]
-            lay = layers[b]
-            ev_qkv, ev_do = [torch.cuda.Event() for _ in range(k)], [torch.cuda.Event() for _ in range(k)]
-            with torch.cuda.stream(s_in):
-                if done[b] is not None:
-                    s_in.wait_event(done[b])
-                for j in range(k):                       # stage-1 order
-                    for dst, src in ((kd, host[1]), (vd, host[2]), (qd, host[0])):
-                        rows(dst, j).copy_(rows(src, j), non_blocking=True)
-                    ev_qkv[j].record(s_in)
-                for j in reversed(range(k)):             # stage-2 order
-                    rows(dod, j).copy_(rows(host[3], j), non_blocking=True)
-                    ev_do[j].record(s_in)
-            if drained[b] is not None:
-                stream.wait_event(drained[b])
-            qv, kv, vv, dov = (t.transpose(0, 1) for t in (qd, kd, vd, dod))
-            lay.dkv.zero_()
-            ev_out = {}
-            for n_op, op in enumerate(order):
-                j = op[1]
-                if op[0] == "f":
-                    if n_op < k:                         # stage 1: chunk j's K, V, Q have arrived
-                        stream.wait_event(ev_qkv[j])
-                    lay.forward_chunk(qv, kv, vv, j, chained=op[2])
-                elif op[0] == "b":
-                    stream.wait_event(ev_do[j])
-                    lay.backward_chunk(qv, kv, vv, dov, j, gamma, sscale)
-                else:
-                    lay.skip_chunk(j)
-                if op[0] in "bz":
-                    ev_out[j] = torch.cuda.Event()
-                    ev_out[j].record(stream)
-            done[b] = torch.cuda.Event()
-            done[b].record(stream)
-            with torch.cuda.stream(s_out):
-                for j in stage2:
-                    s_out.wait_event(ev_out[j])
-                    d2h_chunk(b, j)
-                drained[b] = torch.cuda.Event()
-                drained[b].record(s_out)
-        s_in.wait_event(drained[(args.steps - 1) % 2])
-        if args.steps > 1:
-            s_in.wait_event(drained[args.steps % 2])
+        ends = e2e_steps(args.steps, max(args.warmup, 1))
+        for ev in ends[-2:]:
+            s_in.wait_event(ev)
         e1.record(s_in)
         torch.cuda.synchronize()
+        # per-step completion intervals (D2H drained -> D2H drained), first one from e0
+        e2e_per_step = [e0.elapsed_time(ends[0])] + [ends[i - 1].elapsed_time(ends[i]) for i in range(1, len(ends))]
+        e2e_per_step = [max_over_ranks(v, coll_dev) for v in e2e_per_step]
         ems = max_over_ranks(e0.elapsed_time(e1), coll_dev)
         e2e = {"value": total_flops / (ems / args.steps * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "ms_per_step": ems / args.steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ems / args.steps, "ms_per_step_median": statistics.median(e2e_per_step),
+               "ms_per_step_min": min(e2e_per_step), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "pinned host Q,K,V,dO ([S][h][d]) -> device per chunk in the order the step consumes "
                        "them (copy stream); SeCO/SpaCO chunk calls via the C ABI, each waiting only for its "
                        "chunk's inputs; dQ_j, dKV slot j -> pinned host as soon as chunk j's backward (or "
-                       "skip) is done (copy stream, dKV slot as one 2-D copy); steps double-buffered"}
+                       "skip) is done (copy stream, dKV slot as one 2-D copy); steps double-buffered; W untimed "
+                       "warm-up steps of the same pipeline first; per-step times = intervals between "
+                       "consecutive steps' D2H completions"}
         del sets, layers
 
     cpu = None

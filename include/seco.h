@@ -176,14 +176,20 @@ seco_status spaco_sample_and_scale(int32_t k, int32_t t, uint64_t seed, float ca
  * Layouts: X [rows][n_in], dY [rows][n_out] row-major, row strides ldx, ldy in
  * elements (>= n_in, n_out); A [n_in][rank] and B [rank][n_out] dense, all of
  * `dtype` (SECO_BF16 or SECO_FP32_DEBUG).  n_in, n_out, ldx, ldy must be multiples
- * of one 16-B vector (8 bf16 / 4 fp32 elements) and x, dy, a, b 16-B aligned.  Fixed
- * summation order: deterministic.  Errors: SECO_ERR_ARG (null pointer, non-positive
- * size, short or misaligned stride, workspace too small, unknown dtype),
- * SECO_ERR_UNSUPPORTED (rank not in {1, 2, 4, 8, 16}). */
+ * of one 16-B vector (8 bf16 / 4 fp32 elements) and x, dy, a, b, da, db 16-B aligned.
+ * Summation order: bf16 with n_in, n_out multiples of 64 (128 at rank 16) up to 4096
+ * runs one fused kernel whose per-cluster partial sums reach dA / dB by TMA reduce-add
+ * (order of the clusters unfixed: results may differ in the last bits between calls);
+ * flags = SECO_FLAG_DETERMINISTIC adds them in a fixed order instead (one more
+ * launch).  Every other shape / dtype uses fixed-order kernels in either mode.
+ * Errors: SECO_ERR_ARG (null pointer, non-positive size, short or misaligned stride,
+ * workspace too small, unknown dtype), SECO_ERR_UNSUPPORTED (rank not in
+ * {1, 2, 4, 8, 16}). */
 typedef struct {
   int32_t rows, n_in, n_out, rank;
   seco_dtype dtype;
   int64_t ldx, ldy;
+  int32_t flags;            /* SECO_FLAG_DETERMINISTIC or 0 */
 } seco_lora_shape;
 
 /* Bytes of device workspace seco_lora_grad needs. */

@@ -35,7 +35,8 @@ SECO_FLAG_PREV_INDEPENDENT = 2
 
 class LoraShape(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int32), ("n_in", ctypes.c_int32), ("n_out", ctypes.c_int32),
-                ("rank", ctypes.c_int32), ("dtype", ctypes.c_int32), ("ldx", ctypes.c_int64), ("ldy", ctypes.c_int64)]
+                ("rank", ctypes.c_int32), ("dtype", ctypes.c_int32), ("ldx", ctypes.c_int64), ("ldy", ctypes.c_int64),
+                ("flags", ctypes.c_int32)]
 
 
 class SecoError(RuntimeError):

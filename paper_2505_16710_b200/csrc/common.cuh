@@ -155,6 +155,25 @@ SECO_DEV void mbar_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// Cheap cross-CTA hand-off of shared-memory data (round 2): `.release.cluster` on an arrive and
+// `.acquire.cluster` on a wait compile to MEMBAR.ALL.GPU (+ ERRBAR, CGAERRBAR) and CCTL.IVALL --
+// ~1000 cycles per arrive while global traffic is in flight (tools/trace_lora.py).  When the data
+// handed over lives in shared memory only, a fence restricted to shared memory (MEMBAR.ALL.CTA)
+// before relaxed arrives, and a shared::cluster acquire fence after a relaxed wait, suffice.
+SECO_DEV void fence_release_smem_cluster() {
+  asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+}
+SECO_DEV void fence_acquire_smem_cluster() {
+  asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
+}
+SECO_DEV void mbar_arrive_remote_relaxed(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+// remote arrive with the default semantics (release at CTA scope: no memory fence in SASS), for
+// hand-offs ordered by other means (tcgen05 fences for TMEM, as CUTLASS's cluster pipelines do)
+SECO_DEV void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 SECO_DEV bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(

@@ -70,6 +70,7 @@ inline cudaError_t ensure_smem_attr(Kernel kern, int bytes, std::atomic<unsigned
 struct LoraGeom {
   int rows, n_in, n_out, rank;
   int64_t ldx, ldy;
+  int deterministic;
 };
 size_t lora_ws_floats(const LoraGeom& g);
 cudaError_t launch_lora_grad(const LoraGeom& g, bool bf16, const void* x, const void* dy, const void* a,

@@ -12,6 +12,7 @@
 //          of those rows staged in smem); per-split partial sums of dA / dB to the workspace
 //   reduce partials added in split order into dA / dB
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -594,6 +595,449 @@ constexpr size_t grad_smem() {
 }
 }  // namespace lora_tc
 
+// ============================================================================ fused persistent path
+// lora_fused_kernel: one launch that reads X and dY exactly once (round 2).  A
+// cluster of CS CTAs splits the columns: CTA r of a cluster owns columns [r n_in / CS, ...) of X
+// and [r n_out / CS, ...) of dY, so the A / B slices it contracts against stay in registers for
+// the whole launch and its share of dA / dB accumulates in registers too.  Clusters are
+// persistent (as many as are co-resident) and walk contiguous ranges of 16-row blocks.  Per block:
+//   1. a producer warp streams the CTA's 16 X rows and 16 dY rows (one row per lane, 1-D bulk
+//      copies) into a STAGES-deep ring, completing on an mbarrier;
+//   2. the NW compute warps form the CTA's partial t = X A and u = dY B^T over its columns
+//      (mma.sync m16n8k16, ldmatrix from the ring), sum them across warps, and push the CTA
+//      partial into slot [rank] of every peer's receive buffer with st.async (remote shared-
+//      memory stores that complete_tx on the peer's mbarrier: no cross-CTA round trip);
+//   3. once the CS partials have landed, every lane sums the values its mma fragments need in
+//      rank order (so every CTA sees bit-identical t, u; rank 0 writes u_out), splits them into
+//      bf16 hi + lo (x = hi + lo to 2^-16) and adds X^T u and dY^T t for its columns -- from the
+//      same ring stage, so nothing is read twice -- into its register accumulators.
+// The receive buffers alternate between blocks; a peer can refill one only after it received
+// this CTA's partial of the next block, which this CTA sends after it finished reading it.
+// At the end each CTA writes its dA / dB share to the workspace ([cluster][n_in + n_out][R]),
+// publishes a per-launch epoch flag, and -- once the CTAs of its rank in every cluster have
+// published -- adds the ncl cluster partials of its share of the rank's columns in cluster order
+// into dA / dB: deterministic, no atomics, one launch.
+// R <= 8: clusters of 4 with 16 compute warps (1024 columns of X and dY per CTA); R = 16 (twice
+// the registers per fragment): clusters of 8 with 8 compute warps.
+namespace lora_fz {
+constexpr int kRB = 16;                      // rows per block (one m16 tile)
+constexpr int KW = 4;                        // k16 steps (pass 1) / m16 tiles (pass 2) per warp
+constexpr int kMaxN = 4096;                  // n_in, n_out bound of the fused path
+constexpr int kMaxClusters = 40;             // workspace bound (148 SMs: at most 37 clusters of 4)
+
+template <int R> struct Cfg {
+  static constexpr int CS = R > 8 ? 8 : 4;                  // CTAs per cluster
+  static constexpr int NW = R > 8 ? 8 : 16;                 // compute warps
+  static constexpr int kThreads = 32 * (NW + 1);            // + one producer warp
+  static constexpr int STAGES = R > 8 ? 4 : 3;
+  static constexpr int NT = (R + 7) / 8, RP = 8 * NT;
+  static constexpr int NE = 2 * kRB * RP;                   // t and u of one block
+  static_assert(kMaxN / CS == 16 * NW * KW, "columns per CTA = k16 steps of the warps");
+};
+
+struct Args {
+  const __nv_bfloat16 *x, *dy, *a, *b;
+  int64_t ldx, ldy;
+  int rows, n_in, n_out, nblk, ncl;
+  float* u;                                  // u_out [rows][R]
+  float* part;                               // deterministic: [ncl][n_in R | R n_out] cluster partials
+  float *da, *db;                            // accumulators
+  int deterministic;
+};
+
+#ifdef SECO_LORA_TRACE
+// experiment build only (SECO_DEFINES=-DSECO_LORA_TRACE=1): clock64 per phase and block of CTA 0
+constexpr int kTrBlocks = 32, kTrPts = 12;
+__device__ unsigned long long g_lora_trace[kTrBlocks * kTrPts];
+#define LTRACE(pt, i)                                                                        \
+  do {                                                                                       \
+    if (blockIdx.x == 0 && (i) < kTrBlocks) g_lora_trace[(i) * kTrPts + (pt)] = clock64();   \
+  } while (0)
+#else
+#define LTRACE(pt, i) do { } while (0)
+#endif
+
+// remote shared-memory store of 16 B whose bytes complete_tx on the destination CTA's mbarrier
+SECO_DEV void st_async_v4(uint32_t dst_cluster, float4 v, uint32_t bar_cluster) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+               ::"r"(dst_cluster), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar_cluster)
+               : "memory");
+}
+
+template <int R>
+inline size_t smem_bytes(int n_in, int n_out) {
+  using C = Cfg<R>;
+  const size_t stage = (size_t)kRB * ((n_in / C::CS) * 2 + 16 + (n_out / C::CS) * 2 + 16);
+  return C::STAGES * stage + (size_t)(C::NW + 2 * C::CS + 1) * C::NE * 4 + (2 * C::STAGES + 2) * 8;
+}
+
+template <int R>
+__global__ void __launch_bounds__(Cfg<R>::kThreads, 1) lora_fused_kernel(const Args p) {
+  using lora_tc::ldsm_x4;
+  using lora_tc::ldsm_x4_t;
+  using lora_tc::mma16816;
+  using lora_tc::split2;
+  using C = Cfg<R>;
+  constexpr int CS = C::CS, NW = C::NW, STAGES = C::STAGES, NT = C::NT, RP = C::RP, NE = C::NE;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, q = lane % 4;
+  const int rank = (int)cluster_ctarank();
+  const int cl = (int)blockIdx.x / CS;
+  const int cx = p.n_in / CS, cy = p.n_out / CS;             // columns of this CTA
+  const int colx = rank * cx, coly = rank * cy;
+  const int rsx = cx * 2 + 16, rsy = cy * 2 + 16;            // staged row bytes (+16: ldmatrix banks)
+  const int stage_bytes = kRB * (rsx + rsy);
+  const uint32_t ring = smem_u32(smem);
+  float* wpart = reinterpret_cast<float*>(smem + STAGES * stage_bytes);    // [NW][NE]
+  float* recv = wpart + NW * NE;                                            // [2][CS][NE]
+  float* tu = recv + 2 * CS * NE;                                           // [t | u][n][row]
+  const uint32_t bar0 = smem_u32(tu + NE);
+  auto full = [&](int s) { return bar0 + 8u * s; };
+  auto empty = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto rfull = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
+  const int b0 = cl * p.nblk / p.ncl, nb = (cl + 1) * p.nblk / p.ncl - b0;
+
+  if (threadIdx.x == 0) LTRACE(10, 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(full(s), 1); mbar_init(empty(s), NW); }
+    mbar_init(rfull(0), 1);
+    mbar_init(rfull(1), 1);
+    fence_barrier_init();
+  }
+  cluster_sync();                            // every peer's barriers exist before the first remote store
+
+  if (warp == NW) {
+    // ------------------------------------------------------------ producer: one row per lane
+    const int r = lane % kRB;
+    const bool isy = lane >= kRB;
+    const int bytes = isy ? cy * 2 : cx * 2;
+    for (int i = 0; i < nb; ++i) {
+      const int s = i % STAGES;
+      const int row0 = (b0 + i) * kRB;
+      const int nvalid = min(kRB, p.rows - row0);
+      if (lane == 0) mbar_wait(empty(s), ((i / STAGES) & 1) ^ 1);
+      __syncwarp();
+      const uint32_t dst = ring + s * stage_bytes + (isy ? kRB * rsx + r * rsy : r * rsx);
+      if (r >= nvalid) {                     // ragged tail: zero rows
+        for (int o = 0; o < bytes; o += 16) st_shared_v4(dst + o, 0u, 0u, 0u, 0u);
+        fence_async_smem();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(full(s), (uint32_t)nvalid * (cx + cy) * 2);
+      __syncwarp();
+      if (lane == 0) LTRACE(7, i);
+      if (r < nvalid) {
+        const __nv_bfloat16* src = isy ? p.dy + (int64_t)(row0 + r) * p.ldy + coly
+                                       : p.x + (int64_t)(row0 + r) * p.ldx + colx;
+        bulk_load(dst, src, (uint32_t)bytes, full(s));
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ compute warps
+    const int tid = threadIdx.x;
+    const int nkx = cx / 16, nky = cy / 16;  // k16 steps of pass 1 = m16 tiles of pass 2
+    // pass-1 B fragments (lane (g, q): k = 16 ks + {2q, 2q+1} / {2q+8, 2q+9}, n = 8 nt + g):
+    // A [n_in][R] for t = X A, B^T for u = dY B^T; columns n >= R stay zero
+    uint32_t fa[KW][NT][2], fb[KW][NT][2];
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+      const int ks = warp + NW * kk;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int n = 8 * nt + g;
+        fa[kk][nt][0] = fa[kk][nt][1] = fb[kk][nt][0] = fb[kk][nt][1] = 0u;
+        if (n < R && ks < nkx) {
+          const __nv_bfloat16* ap = p.a + (int64_t)(colx + 16 * ks + 2 * q) * R + n;
+          fa[kk][nt][0] = (uint32_t)__bfloat16_as_ushort(ap[0]) | ((uint32_t)__bfloat16_as_ushort(ap[R]) << 16);
+          fa[kk][nt][1] = (uint32_t)__bfloat16_as_ushort(ap[8 * R]) | ((uint32_t)__bfloat16_as_ushort(ap[9 * R]) << 16);
+        }
+        if (n < R && ks < nky) {
+          const __nv_bfloat16* bp = p.b + (int64_t)n * p.n_out + coly + 16 * ks + 2 * q;
+          fb[kk][nt][0] = *reinterpret_cast<const uint32_t*>(bp);
+          fb[kk][nt][1] = *reinterpret_cast<const uint32_t*>(bp + 8);
+        }
+      }
+    }
+    float accA[KW][NT][4], accB[KW][NT][4];
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) accA[kk][nt][e] = accB[kk][nt][e] = 0.f;
+    if (tid == 0) LTRACE(10, 1);
+    const int li = lane / 8, lr = lane % 8;
+    const uint32_t offx = (uint32_t)((lane % 16) * rsx + (lane / 16) * 16);    // ldmatrix (rows = M)
+    const uint32_t offy = (uint32_t)((lane % 16) * rsy + (lane / 16) * 16);
+    const uint32_t toffx = (uint32_t)((8 * (li / 2) + lr) * rsx + 8 * (li % 2) * 2);   // .trans (rows = K)
+    const uint32_t toffy = (uint32_t)((8 * (li / 2) + lr) * rsy + 8 * (li % 2) * 2);
+    const uint32_t recv_a = smem_u32(recv);
+    for (int i = 0; i < nb; ++i) {
+      const int s = i % STAGES, pb = i & 1;
+      const int row0 = (b0 + i) * kRB;
+      const uint32_t xs = ring + s * stage_bytes, ys = xs + kRB * rsx;
+      if (tid == 0) mbar_expect_tx(rfull(pb), (uint32_t)(CS * NE * 4));   // this block's CS partials
+      mbar_wait(full(s), (i / STAGES) & 1);
+      if (tid == 0) LTRACE(0, i);
+      // pass 1: this warp's share of the CTA partial of t and u
+      float ct[NT][4], cu[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ct[nt][e] = cu[nt][e] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KW; ++kk) {
+        const int ks = warp + NW * kk;
+        uint32_t a0, a1, a2, a3;
+        if (ks < nkx) {
+          ldsm_x4(xs + offx + ks * 32, a0, a1, a2, a3);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma16816(ct[nt], a0, a1, a2, a3, fa[kk][nt][0], fa[kk][nt][1]);
+        }
+        if (ks < nky) {
+          ldsm_x4(ys + offy + ks * 32, a0, a1, a2, a3);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma16816(cu[nt], a0, a1, a2, a3, fb[kk][nt][0], fb[kk][nt][1]);
+        }
+      }
+      if (tid == 0) LTRACE(1, i);
+      float* wp = wpart + warp * NE;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c0 = 8 * nt + 2 * q;
+        *reinterpret_cast<float2*>(wp + g * RP + c0) = make_float2(ct[nt][0], ct[nt][1]);
+        *reinterpret_cast<float2*>(wp + (g + 8) * RP + c0) = make_float2(ct[nt][2], ct[nt][3]);
+        *reinterpret_cast<float2*>(wp + kRB * RP + g * RP + c0) = make_float2(cu[nt][0], cu[nt][1]);
+        *reinterpret_cast<float2*>(wp + kRB * RP + (g + 8) * RP + c0) = make_float2(cu[nt][2], cu[nt][3]);
+      }
+      named_bar_sync(1, 32 * NW);
+      if (tid == 0) LTRACE(2, i);
+      // CTA partial (warps summed in order), 4 values per thread, pushed to slot [rank] of
+      // every peer's receive buffer (this CTA's own included)
+      static_assert(NE / 4 <= 32 * NW, "one float4 of the CTA partial per thread");
+      if (tid < NE / 4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const float4 x = reinterpret_cast<const float4*>(wpart + w * NE)[tid];
+          v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+        }
+        const uint32_t dst = recv_a + (uint32_t)((pb * CS + rank) * NE + 4 * tid) * 4u;
+#pragma unroll
+        for (int c = 0; c < CS; ++c) st_async_v4(mapa_shared(dst, (uint32_t)c), v, mapa_shared(rfull(pb), (uint32_t)c));
+      }
+      if (tid == 0) LTRACE(3, i);
+      // acquire at cluster scope: the peers' stores (and, through them, their reads of the
+      // buffer this block's stores may reuse two blocks later) are ordered before what follows
+      mbar_wait_cluster(rfull(pb), (i >> 1) & 1);
+      if (tid == 0) LTRACE(4, i);
+      // t, u of the block: the CS partials summed in rank order, once per value (every CTA of the
+      // cluster forms bit-identical sums); stored n-major so a lane's fragment rows are adjacent
+      for (int e = tid; e < NE; e += 32 * NW) {
+        const float* rb = recv + pb * CS * NE;
+        float v = 0.f;
+#pragma unroll
+        for (int c = 0; c < CS; ++c) v += rb[c * NE + e];
+        const int isu = e / (kRB * RP), row = (e / RP) % kRB, n = e % RP;
+        tu[isu * kRB * RP + n * kRB + row] = v;
+        if (isu && rank == 0 && n < R && row0 + row < p.rows) p.u[(int64_t)(row0 + row) * R + n] = v;
+      }
+      named_bar_sync(1, 32 * NW);
+      // pass 2 B fragments: u (for X^T u) and t (for dY^T t); k = row, n = rank; hi + lo
+      uint32_t fu[NT][4], ft[NT][4];   // {hi0, hi1, lo0, lo1}
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int n = 8 * nt + g;
+        const float2 t01 = *reinterpret_cast<const float2*>(tu + n * kRB + 2 * q);
+        const float2 t89 = *reinterpret_cast<const float2*>(tu + n * kRB + 2 * q + 8);
+        const float2 u01 = *reinterpret_cast<const float2*>(tu + kRB * RP + n * kRB + 2 * q);
+        const float2 u89 = *reinterpret_cast<const float2*>(tu + kRB * RP + n * kRB + 2 * q + 8);
+        split2(u01.x, u01.y, fu[nt][0], fu[nt][2]);
+        split2(u89.x, u89.y, fu[nt][1], fu[nt][3]);
+        split2(t01.x, t01.y, ft[nt][0], ft[nt][2]);
+        split2(t89.x, t89.y, ft[nt][1], ft[nt][3]);
+      }
+      if (tid == 0) LTRACE(5, i);
+#pragma unroll
+      for (int kk = 0; kk < KW; ++kk) {
+        const int mt = warp + NW * kk;
+        uint32_t a0, a1, a2, a3;
+        if (mt < nkx) {
+          ldsm_x4_t(xs + toffx + mt * 32, a0, a1, a2, a3);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma16816(accA[kk][nt], a0, a1, a2, a3, fu[nt][0], fu[nt][1]);
+            mma16816(accA[kk][nt], a0, a1, a2, a3, fu[nt][2], fu[nt][3]);
+          }
+        }
+        if (mt < nky) {
+          ldsm_x4_t(ys + toffy + mt * 32, a0, a1, a2, a3);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma16816(accB[kk][nt], a0, a1, a2, a3, ft[nt][0], ft[nt][1]);
+            mma16816(accB[kk][nt], a0, a1, a2, a3, ft[nt][2], ft[nt][3]);
+          }
+        }
+      }
+      __syncwarp();
+      if (tid == 0) LTRACE(6, i);
+      if (lane == 0) mbar_arrive(empty(s));
+    }
+    if (tid == 0) LTRACE(11, 0);
+    // this cluster's share of dA (columns of X, [col][R] as in dA) and dB (columns of dY,
+    // [R][col] as in dB), staged in the (now idle) ring and moved with 1-D bulk copies: 1 + R
+    // contiguous runs.  Default: TMA reduce-add straight into dA / dB (cluster order unfixed,
+    // like the attention backward's dQ / dKV deposits).  Deterministic: the runs go to the
+    // workspace and lora_fused_reduce_kernel adds the clusters in order.
+    named_bar_sync(1, 32 * NW);                               // every warp is done with the ring
+    float* stg = reinterpret_cast<float*>(smem);              // [cx][R] | [R][cy]
+    float* stgy = stg + cx * R;
+#pragma unroll
+    for (int kk = 0; kk < KW; ++kk) {
+      const int mt = warp + NW * kk;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int k = 8 * nt + 2 * q + e;
+            if (k >= R) continue;
+            if (mt < nkx) stg[(16 * mt + g + 8 * h) * R + k] = accA[kk][nt][2 * h + e];
+            if (mt < nky) stgy[k * cy + 16 * mt + g + 8 * h] = accB[kk][nt][2 * h + e];
+          }
+    }
+    fence_async_smem();                                       // generic smem writes -> bulk copies
+    named_bar_sync(1, 32 * NW);
+    if (tid == 0) {
+      float* oa = p.deterministic ? p.part + (int64_t)cl * (p.n_in + p.n_out) * R : p.da;
+      float* ob = p.deterministic ? oa + (int64_t)p.n_in * R : p.db;
+      if (p.deterministic) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(oa + (int64_t)colx * R), "r"(smem_u32(stg)), "r"(cx * R * 4) : "memory");
+        for (int k = 0; k < R; ++k)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       ::"l"(ob + (int64_t)k * p.n_out + coly), "r"(smem_u32(stgy + k * cy)), "r"(cy * 4) : "memory");
+      } else {
+        bulk_reduce_add_f32(oa + (int64_t)colx * R, smem_u32(stg), cx * R * 4);
+        for (int k = 0; k < R; ++k) bulk_reduce_add_f32(ob + (int64_t)k * p.n_out + coly, smem_u32(stgy + k * cy), cy * 4);
+      }
+      bulk_commit();
+      bulk_wait0();
+      LTRACE(11, 1);
+    }
+  }
+  cluster_sync();                            // no CTA leaves while a peer may still store into it
+}
+
+// Deterministic mode: dA / dB (as one flat [n_in R | R n_out] array) += the ncl cluster partials
+// in a fixed association -- thread row cr takes clusters cr, cr + 8, ... in order, then the 8 row
+// sums in row order.  Launched with programmatic stream serialization behind the fused kernel.
+__global__ void __launch_bounds__(256) lora_fused_reduce_kernel(const float* __restrict__ part, int n_a, int n_b,
+                                                                int ncl, float* __restrict__ dA, float* __restrict__ dB) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // the fused kernel's partials are complete
+  constexpr int G = 32, CR = 8, MAXC = (kMaxClusters + CR - 1) / CR;
+  __shared__ float4 red[CR][G];
+  const int n = n_a + n_b;                             // floats; n_a, n_b multiples of 4
+  const int gi = threadIdx.x % G, cr = threadIdx.x / G;
+  const int e = (blockIdx.x * G + gi) * 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e < n) {
+    float4 v[MAXC];
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m)
+      if (cr + CR * m < ncl) v[m] = *reinterpret_cast<const float4*>(part + (int64_t)(cr + CR * m) * n + e);
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m)
+      if (cr + CR * m < ncl) { acc.x += v[m].x; acc.y += v[m].y; acc.z += v[m].z; acc.w += v[m].w; }
+  }
+  red[cr][gi] = acc;
+  __syncthreads();
+  if (cr == 0 && e < n) {
+#pragma unroll
+    for (int r = 1; r < CR; ++r) {
+      const float4 x = red[r][gi];
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    float4* d = e < n_a ? reinterpret_cast<float4*>(dA + e) : reinterpret_cast<float4*>(dB + (e - n_a));
+    float4 o = *d;
+    o.x += acc.x; o.y += acc.y; o.z += acc.z; o.w += acc.w;
+    *d = o;
+  }
+}
+}  // namespace lora_fz
+
+#ifdef SECO_LORA_TRACE
+extern "C" int seco_debug_lora_trace(unsigned long long* host, int n) {
+  const int m = n < lora_fz::kTrBlocks * lora_fz::kTrPts ? n : lora_fz::kTrBlocks * lora_fz::kTrPts;
+  return (int)cudaMemcpyFromSymbol(host, lora_fz::g_lora_trace, m * sizeof(unsigned long long));
+}
+#endif
+
+bool lora_fused_ok(const LoraGeom& g) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("SECO_LORA_FUSED");  // A/B switch: SECO_LORA_FUSED=0 selects the 2-pass kernels
+    return e == nullptr || e[0] != '0';
+  }();
+  const int cs = g.rank > 8 ? 8 : 4;
+  return enabled && g.n_in % (16 * cs) == 0 && g.n_out % (16 * cs) == 0 && g.n_in <= lora_fz::kMaxN &&
+         g.n_out <= lora_fz::kMaxN && g.ldx % 8 == 0 && g.ldy % 8 == 0 &&
+         (g.rank == 1 || g.rank == 2 || g.rank == 4 || g.rank == 8 || g.rank == 16);
+}
+
+size_t lora_fused_ws_floats(const LoraGeom& g) {   // deterministic mode's cluster partials
+  return (size_t)lora_fz::kMaxClusters * (g.n_in + g.n_out) * g.rank;
+}
+
+template <int R>
+static cudaError_t launch_lora_fused(const LoraGeom& g, const void* x, const void* dy, const void* a, const void* b,
+                                     float* da, float* db, float* u, float* ws, cudaStream_t st) {
+  using namespace lora_fz;
+  using C = Cfg<R>;
+  const int max_smem = (int)smem_bytes<R>(kMaxN, kMaxN);
+  static std::atomic<unsigned long long> attr_done{0};
+  cudaError_t e = ensure_smem_attr(lora_fused_kernel<R>, max_smem, attr_done);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute cattr[1];
+  cattr[0].id = cudaLaunchAttributeClusterDimension;
+  cattr[0].val.clusterDim.x = C::CS; cattr[0].val.clusterDim.y = 1; cattr[0].val.clusterDim.z = 1;
+  // persistent clusters: as many as are co-resident (queried once per device at the largest
+  // shared-memory footprint, so a smaller shape never exceeds it)
+  static std::atomic<int> max_cl[64];
+  int dev = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  int ncl = max_cl[dev & 63].load(std::memory_order_relaxed);
+  if (ncl == 0) {
+    cudaLaunchConfig_t qc = {};
+    qc.gridDim = dim3(C::CS * kMaxClusters); qc.blockDim = dim3(C::kThreads); qc.dynamicSmemBytes = max_smem;
+    qc.attrs = cattr; qc.numAttrs = 1;
+    if ((e = cudaOccupancyMaxActiveClusters(&ncl, lora_fused_kernel<R>, &qc)) != cudaSuccess) return e;
+    ncl = ncl < 1 ? 1 : (ncl > kMaxClusters ? kMaxClusters : ncl);
+    max_cl[dev & 63].store(ncl, std::memory_order_relaxed);
+    if (std::getenv("SECO_LORA_DEBUG")) fprintf(stderr, "lora_fused: %d co-resident clusters of %d\n", ncl, C::CS);
+  }
+  Args p;
+  p.x = static_cast<const __nv_bfloat16*>(x); p.dy = static_cast<const __nv_bfloat16*>(dy);
+  p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
+  p.ldx = g.ldx; p.ldy = g.ldy; p.rows = g.rows; p.n_in = g.n_in; p.n_out = g.n_out;
+  p.nblk = (g.rows + kRB - 1) / kRB;
+  p.ncl = ncl < p.nblk ? ncl : p.nblk;
+  p.u = u; p.part = ws; p.da = da; p.db = db; p.deterministic = g.deterministic;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C::CS * p.ncl); cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = smem_bytes<R>(g.n_in, g.n_out); cfg.stream = st;
+  cfg.attrs = cattr; cfg.numAttrs = 1;
+  if ((e = cudaLaunchKernelEx(&cfg, lora_fused_kernel<R>, p)) != cudaSuccess || !g.deterministic) return e;
+  // deterministic: cluster partials -> dA, dB in cluster order (its launch overlaps the tail)
+  cudaLaunchAttribute rattr[1];
+  rattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  rattr[0].val.programmaticStreamSerializationAllowed = 1;
+  const int n = (g.n_in + g.n_out) * R;
+  cudaLaunchConfig_t rc = {};
+  rc.gridDim = dim3((n / 4 + 31) / 32); rc.blockDim = dim3(256); rc.stream = st; rc.attrs = rattr; rc.numAttrs = 1;
+  return cudaLaunchKernelEx(&rc, lora_fused_reduce_kernel, (const float*)ws, g.n_in * R, g.n_out * R, p.ncl, da, db);
+}
+
 bool lora_tc_ok(const LoraGeom& g) {
   static const bool enabled = [] {
     const char* e = std::getenv("SECO_LORA_TC");     // A/B switch: SECO_LORA_TC=0 selects the CUDA-core kernels
@@ -606,7 +1050,9 @@ bool lora_tc_ok(const LoraGeom& g) {
 
 size_t lora_tc_ws_floats(const LoraGeom& g) {
   const int nt = g.rank > 8 ? 2 : 1;
-  return (size_t)2 * ((g.rows + 15) / 16) * nt * 32 * 4;
+  const size_t tc = (size_t)2 * ((g.rows + 15) / 16) * nt * 32 * 4;
+  const size_t fz = lora_fused_ws_floats(g);
+  return tc > fz ? tc : fz;
 }
 
 template <int R>
@@ -650,6 +1096,16 @@ static cudaError_t launch_lora_t(const LoraGeom& g, const void* x, const void* d
 cudaError_t launch_lora_grad(const LoraGeom& g, bool bf16, const void* x, const void* dy, const void* a,
                              const void* b, float* da, float* db, float* u, float* ws, cudaStream_t st,
                              int* launches) {
+  if (bf16 && lora_fused_ok(g)) {
+    *launches = g.deterministic ? 2 : 1;
+    switch (g.rank) {
+      case 1: return launch_lora_fused<1>(g, x, dy, a, b, da, db, u, ws, st);
+      case 2: return launch_lora_fused<2>(g, x, dy, a, b, da, db, u, ws, st);
+      case 4: return launch_lora_fused<4>(g, x, dy, a, b, da, db, u, ws, st);
+      case 8: return launch_lora_fused<8>(g, x, dy, a, b, da, db, u, ws, st);
+      default: return launch_lora_fused<16>(g, x, dy, a, b, da, db, u, ws, st);
+    }
+  }
   if (bf16 && lora_tc_ok(g)) {
     *launches = 2;
     switch (g.rank) {

@@ -345,6 +345,7 @@ static bool lora_geom(const seco_lora_shape* s, seco::LoraGeom* g) {
   if (!s || s->rows <= 0 || s->n_in <= 0 || s->n_out <= 0 || s->rank <= 0) return false;
   g->rows = s->rows; g->n_in = s->n_in; g->n_out = s->n_out; g->rank = s->rank;
   g->ldx = s->ldx; g->ldy = s->ldy;
+  g->deterministic = (s->flags & SECO_FLAG_DETERMINISTIC) != 0;
   return true;
 }
 

@@ -93,7 +93,7 @@ class _LoRAProj(torch.autograd.Function):
         m, li, name = ctx.model, ctx.li, ctx.name
         dy = dy.contiguous()
         u = torch.empty(x.shape[0], A.shape[1], dtype=torch.float32, device=x.device)
-        shape = ops.lora_shape(x, dy, A.shape[1])
+        shape = ops.lora_shape(x, dy, A.shape[1], deterministic=m.deterministic)
         ws = m._lora_ws(ops.seco_lora_workspace_size(shape))
         dA, dB = m.lora_views[li]["A" + name], m.lora_views[li]["B" + name]
         ops.seco_lora_grad(shape, x, dy, A, B, dA, dB, u, ws)
@@ -135,6 +135,7 @@ class ChunkedLoRAStack:
         self.reducer = LayerBucketReducer()
         self._final_chunk = False
         self._pending = [0] * len(self.params)
+        self.deterministic = deterministic
         self.state = [_LayerState(hq, hkv, d, seq, chunk, dtype, self.device, deterministic) for _ in layers]
         half = d // 2
         inv = rope_base ** (-torch.arange(half, dtype=torch.float64) * 2.0 / d)

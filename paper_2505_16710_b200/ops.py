@@ -95,13 +95,15 @@ def last_launch_count() -> int:
     return int(load().seco_last_launch_count())
 
 
-def lora_shape(x, dy, rank: int) -> LoraShape:
-    """Shape record for X [rows][n_in], dY [rows][n_out] (row-major, unit inner stride)."""
+def lora_shape(x, dy, rank: int, deterministic: bool = False) -> LoraShape:
+    """Shape record for X [rows][n_in], dY [rows][n_out] (row-major, unit inner stride).
+    deterministic: fixed summation order (SECO_FLAG_DETERMINISTIC, include/seco.h)."""
     if x.dtype not in _DTYPES or dy.dtype != x.dtype:
         raise TypeError("x / dy must both be bf16 or float32")
     if x.stride(1) != 1 or dy.stride(1) != 1 or x.shape[0] != dy.shape[0]:
         raise ValueError("x, dy: [rows][n] with contiguous rows and equal row counts")
-    return LoraShape(x.shape[0], x.shape[1], dy.shape[1], rank, _DTYPES[x.dtype], x.stride(0), dy.stride(0))
+    return LoraShape(x.shape[0], x.shape[1], dy.shape[1], rank, _DTYPES[x.dtype], x.stride(0), dy.stride(0),
+                     _lib.SECO_FLAG_DETERMINISTIC if deterministic else 0)
 
 
 def seco_lora_workspace_size(shape: LoraShape) -> int:

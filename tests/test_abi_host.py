@@ -170,7 +170,7 @@ def test_workspace_independent_of_sequence_length(lib):
     (dict(dtype=7), _lib.SECO_ERR_ARG),
 ])
 def test_lora_argument_validation(lib, kw, code):
-    d = dict(rows=64, n_in=32, n_out=48, rank=8, dtype=0, ldx=32, ldy=48)
+    d = dict(rows=64, n_in=32, n_out=48, rank=8, dtype=0, ldx=32, ldy=48, flags=0)
     d.update(kw)
     s = _lib.LoraShape(*[d[f] for f, _ in _lib.LoraShape._fields_])
     dummy = ctypes.c_void_p(1 << 20)

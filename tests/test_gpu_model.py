@@ -119,12 +119,15 @@ def test_bf16_spaco_all_chunks_is_seco():
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("rows,n_in,n_out,r", [(512, 256, 384, 8), (129, 72, 40, 4), (2048, 1024, 1024, 16),
                                               (2048, 4096, 1024, 8), (300, 1024, 512, 4), (64, 256, 256, 1),
-                                              (17, 512, 2048, 2)])
-def test_lora_grad_kernel_matches_oracle(dtype, rows, n_in, n_out, r):
+                                              (17, 512, 2048, 2), (4001, 4096, 4096, 8), (256, 4096, 8192, 8),
+                                              (40, 128, 4096, 16)])
+@pytest.mark.parametrize("det", [False, True])
+def test_lora_grad_kernel_matches_oracle(dtype, rows, n_in, n_out, r, det):
     """seco_lora_grad against oracle.multilayer.lora_grads: dA, dB accumulate (two
     calls give twice the gradient), u = dY B^T; X is a strided view (padded rows).  bf16 with
-    n_in, n_out multiples of 256 takes the tensor-core kernels (ragged row counts included),
-    everything else the CUDA-core ones."""
+    n_in, n_out multiples of 128 up to 4096 takes the fused persistent kernel (ragged row counts
+    and fewer row blocks than clusters included), bf16 multiples of 256 beyond that the two-pass
+    tensor-core kernels (4096 -> 8192), everything else the CUDA-core ones."""
     from paper_2505_16710_b200 import ops
     from synth import round_to_bf16
     rng = np.random.default_rng(rows + r)
@@ -143,11 +146,17 @@ def test_lora_grad_kernel_matches_oracle(dtype, rows, n_in, n_out, r):
     da = torch.zeros(n_in, r, device="cuda")
     db = torch.zeros(r, n_out, device="cuda")
     u = torch.empty(rows, r, device="cuda")
-    shape = ops.lora_shape(x, dy, r)
+    shape = ops.lora_shape(x, dy, r, deterministic=det)
     ws = torch.empty(ops.seco_lora_workspace_size(shape) // 4, device="cuda")
     for _ in range(2):
         ops.seco_lora_grad(shape, x, dy, a, b, da, db, u, ws)
     torch.cuda.synchronize()
+    if det:   # fixed summation order: a repeat from zero reproduces the first call bit for bit
+        da1, db1 = torch.zeros_like(da), torch.zeros_like(db)
+        ops.seco_lora_grad(shape, x, dy, a, b, da1, db1, u, ws)
+        da2, db2 = torch.zeros_like(da), torch.zeros_like(db)
+        ops.seco_lora_grad(shape, x, dy, a, b, da2, db2, u, ws)
+        assert torch.equal(da1, da2) and torch.equal(db1, db2)
     rdA, rdB, ru = (np.asarray(t) for t in __import__("oracle").multilayer.lora_grads(x_np, dy_np, a_np, b_np))
     assert err(da.cpu().numpy(), 2 * rdA) <= 1e-5
     assert err(db.cpu().numpy(), 2 * rdB) <= 1e-5

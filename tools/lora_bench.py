@@ -18,7 +18,7 @@ shapes = [tuple(int(a) for a in sys.argv[1:5])] if len(sys.argv) > 4 else \
 # whose write-back the next kernel pays for (~20 us), a read leaves clean lines
 flush = torch.ones(256 * 1024 * 1024 // 4, device="cuda")
 sink = torch.empty(1, device="cuda")
-for rows, n_in, n_out, r in shapes:
+for (rows, n_in, n_out, r), det in [(sh_, dt_) for sh_ in shapes for dt_ in (False, True)]:
     x = torch.randn(rows, n_in, device="cuda").bfloat16()
     dy = torch.randn(rows, n_out, device="cuda").bfloat16()
     a = torch.randn(n_in, r, device="cuda").bfloat16()
@@ -26,7 +26,7 @@ for rows, n_in, n_out, r in shapes:
     da = torch.zeros(n_in, r, device="cuda")
     db = torch.zeros(r, n_out, device="cuda")
     u = torch.empty(rows, r, device="cuda")
-    sh = ops.lora_shape(x, dy, r)
+    sh = ops.lora_shape(x, dy, r, deterministic=det)
     ws = torch.empty(ops.seco_lora_workspace_size(sh) // 4, device="cuda")
     for _ in range(5):
         ops.seco_lora_grad(sh, x, dy, a, b, da, db, u, ws)
@@ -34,7 +34,7 @@ for rows, n_in, n_out, r in shapes:
     n = 30
     ts = []
     for _ in range(n):
-        torch.sum(flush, dim=0, out=sink)
+        sink.copy_(flush.sum())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         ops.seco_lora_grad(sh, x, dy, a, b, da, db, u, ws)
@@ -44,6 +44,6 @@ for rows, n_in, n_out, r in shapes:
     ts.sort()
     us = ts[len(ts) // 2]
     alg = rows * (n_in + n_out) * 2 + rows * r * 4 + 2 * (n_in + n_out) * r * 4
-    print(f"lora_grad rows={rows} {n_in}->{n_out} r={r}: median {us:.1f} us (min {ts[0]:.1f}), "
+    print(f"lora_grad rows={rows} {n_in}->{n_out} r={r}{' det' if det else ''}: median {us:.1f} us (min {ts[0]:.1f}), "
           f"{alg / 1e6:.1f} MB algorithmic -> {alg / us / 1e3:.0f} GB/s "
           f"({100 * alg / us / 1e3 / 6547.8:.0f}% of 6547.8 measured HBM), launches {ops.last_launch_count()}")
