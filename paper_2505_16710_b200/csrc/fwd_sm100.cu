@@ -43,6 +43,17 @@ constexpr int kEmuPairs = SECO_FWD_EMU;
 #define SECO_FWD_PDL 1
 #endif
 constexpr int kSMs = 148;                  // B200    // of every 16 column pairs, this many use ex2_emu2
+#ifndef SECO_FWD_SPLIT
+#define SECO_FWD_SPLIT 2
+#endif
+#ifndef SECO_FWD_PROD_SLEEP
+#define SECO_FWD_PROD_SLEEP 0
+#endif
+#ifndef SECO_FWD_LSUM_AFTER
+#define SECO_FWD_LSUM_AFTER 0
+#endif
+// P is released to the MMA warp in two parts: 32-key chunks [0, kSplit) and [kSplit, 4)
+constexpr int kSplit = SECO_FWD_SPLIT;
 
 template <int NH, int D, int STAGES>
 struct Layout {
@@ -168,7 +179,13 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       uint32_t phase = 0;
       for (int t = t0; t < t0 + nT; ++t) {
         for (int w = 0; w < 2; ++w) {  // K_t then V_t
+#if SECO_FWD_PROD_SLEEP
+          // the ring runs STAGES / 2 tiles ahead: back off instead of spinning on the issue
+          // slots this warp's SM sub-partition shares with two softmax warps
+          while (!mbar_try_wait(bar_kv_empty(slot), phase ^ 1)) __nanosleep(SECO_FWD_PROD_SLEEP);
+#else
           mbar_wait(bar_kv_empty(slot), phase ^ 1);
+#endif
           mbar_expect_tx(bar_kv_full(slot), L::kTileBytes);
           const CUtensorMap* m = w == 0 ? &tm_k : &tm_v;
           for (int x = 0; x < HALVES; ++x)
@@ -192,11 +209,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
                  idesc_s, kk > 0);
         }
       };
-      auto issue_pv_half = [&](int b, int slot, int hf, bool acc) {   // keys [64 hf, 64 hf + 64)
+      auto issue_pv_half = [&](int b, int slot, int hf, bool acc) {   // part hf: k16 steps [k0, k1)
         const uint32_t va = sKV + slot * L::kTileBytes;
+        const int k0 = hf ? 2 * fwd::kSplit : 0, k1 = hf ? fwd::BN / 16 : 2 * fwd::kSplit;
 #pragma unroll
-        for (int k4 = 0; k4 < fwd::BN / 32; ++k4) {
-          const int kk = hf * (fwd::BN / 32) + k4;
+        for (int kk = k0; kk < k1; ++kk) {
           const uint64_t bd = make_desc_sw128(va + kk * 2048, BOX, 1024);
           mma_ts(tmem + NH * fwd::BN + b * D, tmem + b * fwd::BN + kk * 8, bd, idesc_pv, (acc || kk > 0) ? 1u : 0u);
         }
@@ -301,11 +318,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       // and give exactly 0 through MUFU.
       const f2_t negm = f2(-m_use, -m_use);
       f2_t lsum0 = f2(0.f, 0.f), lsum1 = f2(0.f, 0.f);
-      auto exp_half = [&](int hf, auto emu_pairs) {
+      auto exp_half = [&](int hf, auto emu_pairs) {   // part hf: 32-key chunks [c0, c1)
         constexpr int EMU = decltype(emu_pairs)::value;
+        const int c0 = hf ? fwd::kSplit : 0, c1 = hf ? fwd::BN / 32 : fwd::kSplit;
 #pragma unroll
-        for (int c2 = 0; c2 < 2; ++c2) {
-          const int cc = hf * 2 + c2;
+        for (int cc = c0; cc < c1; ++cc) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -313,7 +330,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
             // EMU of the 16 pairs, evenly spread, run on the FMA pipe (ex2_emu2)
             const bool emu = ((i / 2) * EMU) / 16 != ((i / 2 + 1) * EMU) / 16;
             const f2_t p2 = emu ? ex2_emu2(x) : f2(ex2(f2lo(x)), ex2(f2hi(x)));
+#if SECO_FWD_LSUM_AFTER
+            v[cc * 32 + i] = (uint32_t)p2; v[cc * 32 + i + 1] = (uint32_t)(p2 >> 32);   // row sum after release
+#else
             if ((i / 2) & 1) lsum1 = fadd2(lsum1, p2); else lsum0 = fadd2(lsum0, p2);
+#endif
             pk[i / 2] = pack_bf16_f2(p2);
           }
           tmem_st16(tS + cc * 16, pk);
@@ -330,6 +351,13 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         else exp_half(hf, std::integral_constant<int, fwd::kEmuPairs>{});
       }
       if (lane == 0 && wq == 0) FTRACE(8 + b, t);
+#if SECO_FWD_LSUM_AFTER
+#pragma unroll
+      for (int i = 0; i < fwd::BN; i += 4) {
+        lsum0 = fadd2(lsum0, f2u(v[i], v[i + 1]));
+        lsum1 = fadd2(lsum1, f2u(v[i + 2], v[i + 3]));
+      }
+#endif
       const f2_t lsum = fadd2(lsum0, lsum1);
       l += f2lo(lsum) + f2hi(lsum);
     }
