@@ -44,13 +44,19 @@ constexpr int kEmuPairs = SECO_FWD_EMU;
 #endif
 constexpr int kSMs = 148;                  // B200    // of every 16 column pairs, this many use ex2_emu2
 #ifndef SECO_FWD_SPLIT
-#define SECO_FWD_SPLIT 2
+#define SECO_FWD_SPLIT 3
+#endif
+#ifndef SECO_FWD_MAXCH
+#define SECO_FWD_MAXCH 4
+#endif
+#ifndef SECO_FWD_EMU_MIDDLE
+#define SECO_FWD_EMU_MIDDLE 0
 #endif
 #ifndef SECO_FWD_PROD_SLEEP
 #define SECO_FWD_PROD_SLEEP 0
 #endif
 #ifndef SECO_FWD_LSUM_AFTER
-#define SECO_FWD_LSUM_AFTER 0
+#define SECO_FWD_LSUM_AFTER 1
 #endif
 // P is released to the MMA warp in two parts: 32-key chunks [0, kSplit) and [kSplit, 4)
 constexpr int kSplit = SECO_FWD_SPLIT;
@@ -104,7 +110,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   auto bar_kv_full = [&](int s) { return bar0 + 8u * (NH + s); };
   auto bar_kv_empty = [&](int s) { return bar0 + 8u * (NH + STAGES + s); };
   auto bar_s_full = [&](int b) { return bar0 + 8u * (NH + 2 * STAGES + b); };
-  // p_half(b, 0/1): P_b for keys 0-63 / 64-127 is in TMEM (one arrival per softmax warp)
+  // p_half(b, 0/1): P_b for keys [0, 32 kSplit) / [32 kSplit, 128) is in TMEM (one arrival per
+  // softmax warp)
   auto bar_p_half = [&](int b, int hf) { return bar0 + 8u * (2 * NH + 2 * STAGES + 2 * b + hf); };
   auto bar_o_full = [&](int b) { return bar0 + 8u * (4 * NH + 2 * STAGES + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
@@ -286,14 +293,28 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         for (int i = 0; i < fwd::BN; ++i)
           if (i > r) v[i] = __float_as_uint(-INFINITY);
       }
+#if SECO_FWD_MAXCH == 4
+      // four independent FMNMX3 chains: half the dependent-latency depth of two
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < fwd::BN; i += 8) {
+        mx0 = fmax3(mx0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        mx2 = fmax3(mx2, __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
+        mx3 = fmax3(mx3, __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
+      }
+      mx0 = fmax3(mx0, mx1, fmaxf(mx2, mx3));
+#else
       float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
       for (int i = 0; i < fwd::BN; i += 4) {
         mx0 = fmax3(mx0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
         mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
       }
+      mx0 = fmaxf(mx0, mx1);
+#endif
       if (lane == 0 && wq == 0) FTRACE(6 + b, t);
-      const float m_new = fmaxf(m, fmaxf(mx0, mx1) * sl2);
+      const float m_new = fmaxf(m, mx0 * sl2);
       const bool need = m_new > m + fwd::kRescaleThreshold;
       const float m_use = need ? m_new : m;
       const float alpha = need ? ex2(m - m_new) : 1.f;
@@ -313,7 +334,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       }
       m = m_use;
       // P = exp2(S sigma log2e - m) -> bf16 -> TMEM columns [16cc, 16cc+16) of S_b's block, in two
-      // halves (keys 0-63, 64-127), each released to the MMA warp as soon as it is stored, so
+      // parts (keys [0, 96) and [96, 128) by default), each released to the MMA warp as soon as it is stored, so
       // PV on the first half overlaps the exponentials of the second.  Masked entries hold -inf
       // and give exactly 0 through MUFU.
       const f2_t negm = f2(-m_use, -m_use);
@@ -328,7 +349,12 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           for (int i = 0; i < 32; i += 2) {
             const f2_t x = ffma2(f2u(v[cc * 32 + i], v[cc * 32 + i + 1]), sl2x2, negm);
             // EMU of the 16 pairs, evenly spread, run on the FMA pipe (ex2_emu2)
+#if SECO_FWD_EMU_MIDDLE
+            // FA4's placement: only the middle 32-key chunks, the last EMU of every 8 pairs
+            const bool emu = EMU > 0 && cc > 0 && cc < fwd::BN / 32 - 1 && (i / 2) % 8 >= 8 - EMU;
+#else
             const bool emu = ((i / 2) * EMU) / 16 != ((i / 2 + 1) * EMU) / 16;
+#endif
             const f2_t p2 = emu ? ex2_emu2(x) : f2(ex2(f2lo(x)), ex2(f2hi(x)));
 #if SECO_FWD_LSUM_AFTER
             v[cc * 32 + i] = (uint32_t)p2; v[cc * 32 + i + 1] = (uint32_t)(p2 >> 32);   // row sum after release
