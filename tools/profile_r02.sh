@@ -2,7 +2,7 @@
 # spawn path (plumbing on one GPU), the reference arm, the ncu launch list and full captures of
 # the j = 15 backward and forward launches.  Outputs under gpurun_out/r02_*.
 set -x
-P=gpurun_out/r02
+P=${P:-gpurun_out/r02}    # output prefix
 python bench.py > ${P}_bench_cfg3.json 2> ${P}_bench_cfg3.err
 python bench.py --mode spaco --sampler paper --no-cpu-baseline > ${P}_bench_cfg3_spaco_paper.json 2>&1
 python bench.py --mode spaco --sampler ht --no-cpu-baseline > ${P}_bench_cfg3_spaco_ht.json 2>&1
