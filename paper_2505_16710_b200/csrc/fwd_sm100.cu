@@ -6,7 +6,8 @@
 // group (GQA: the NH tiles share every K/V tile loaded into shared memory).
 // Warp roles (warp-uniform dispatch):
 //   warp 0        TMA producer: Q tiles once, then K_t, V_t through a STAGES-deep ring
-//   warp 1        MMA issuer (one thread): S_b = Q_b K_t^T (SS) and O_b += P_b V_t (TS: P_b
+//   warp 1        MMA issuer (converged warp, one elected lane issues): S_b = Q_b K_t^T (SS) and
+//                 O_b += P_b V_t (TS: P_b
 //                 is read straight from tensor memory)
 //   warp 2        TMEM allocator
 //   warps 4..     one 128-thread softmax warpgroup per q-head tile b (thread = query row):
@@ -45,6 +46,9 @@ constexpr int kEmuPairs = SECO_FWD_EMU;
 constexpr int kSMs = 148;                  // B200    // of every 16 column pairs, this many use ex2_emu2
 #ifndef SECO_FWD_SPLIT
 #define SECO_FWD_SPLIT 3
+#endif
+#ifndef SECO_FWD_MMA_WARP
+#define SECO_FWD_MMA_WARP 1
 #endif
 #ifndef SECO_FWD_MAXCH
 #define SECO_FWD_MAXCH 4
@@ -204,35 +208,45 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+#if SECO_FWD_MMA_WARP
+    // converged warp: every lane waits, one elected lane issues (operands stay warp-uniform)
+    const bool issuer = elect_one_sync();
+    {
+#else
+    const bool issuer = true;
     if (lane == 0) {
+#endif
       constexpr uint32_t idesc_s = make_idesc_bf16(fwd::BM, fwd::BN, 0, 0);  // Q K-major, K K-major
       constexpr uint32_t idesc_pv = make_idesc_bf16(fwd::BM, D, 0, 1);       // P (TMEM) K-major, V MN-major
+      // descriptors: one per tile base; a k-step adds its byte offset / 16 to the 14-bit start
+      // address field (shared-memory offsets stay below 256 KiB, so the field never carries)
       auto issue_s = [&](int b, int slot) {
-        const uint32_t qa = sQ + b * L::kTileBytes, ka = sKV + slot * L::kTileBytes;
+        const uint64_t dq = make_desc_sw128(sQ + b * L::kTileBytes, 16, 1024);
+        const uint64_t dk = make_desc_sw128(sKV + slot * L::kTileBytes, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk / 4) * BOX + (kk % 4) * 32;
-          mma_ss(tmem + b * fwd::BN, make_desc_sw128(qa + off, 16, 1024), make_desc_sw128(ka + off, 16, 1024),
-                 idesc_s, kk > 0);
+          const uint32_t off = ((kk / 4) * BOX + (kk % 4) * 32) >> 4;
+          if (issuer) mma_ss(tmem + b * fwd::BN, dq + off, dk + off, idesc_s, kk > 0);
         }
       };
       auto issue_pv_half = [&](int b, int slot, int hf, bool acc) {   // part hf: k16 steps [k0, k1)
-        const uint32_t va = sKV + slot * L::kTileBytes;
+        const uint64_t dv = make_desc_sw128(sKV + slot * L::kTileBytes, BOX, 1024);
         const int k0 = hf ? 2 * fwd::kSplit : 0, k1 = hf ? fwd::BN / 16 : 2 * fwd::kSplit;
 #pragma unroll
-        for (int kk = k0; kk < k1; ++kk) {
-          const uint64_t bd = make_desc_sw128(va + kk * 2048, BOX, 1024);
-          mma_ts(tmem + NH * fwd::BN + b * D, tmem + b * fwd::BN + kk * 8, bd, idesc_pv, (acc || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = k0; kk < k1; ++kk)
+          if (issuer)
+            mma_ts(tmem + NH * fwd::BN + b * D, tmem + b * fwd::BN + kk * 8, dv + (uint32_t)(kk * 2048 >> 4), idesc_pv,
+                   (acc || kk > 0) ? 1u : 0u);
       };
+      auto commit = [&](uint32_t bar) { if (issuer) mma_commit(bar); };
       for (int b = 0; b < NH; ++b) mbar_wait(bar_q(b), 0);
       int slot = 0;
       uint32_t phase = 0;
       // prologue: S_b(0)
       mbar_wait(bar_kv_full(slot), phase);
       tc_fence_after();
-      for (int b = 0; b < NH; ++b) { issue_s(b, slot); mma_commit(bar_s_full(b)); }
-      mma_commit(bar_kv_empty(slot));
+      for (int b = 0; b < NH; ++b) { issue_s(b, slot); commit(bar_s_full(b)); }
+      commit(bar_kv_empty(slot));
       if (++slot == STAGES) { slot = 0; phase ^= 1; }
       for (int t = 0; t < nT; ++t) {   // t counts this CTA's tiles
         const int vslot = slot;
@@ -251,17 +265,17 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           FTRACE(11 + 3 * b, t);
           tc_fence_after();
           issue_pv_half(b, vslot, 1, true);
-          mma_commit(bar_o_full(b));
+          commit(bar_o_full(b));
           if (more) {
             if (b == 0) { mbar_wait(bar_kv_full(kslot), phase); tc_fence_after(); }
             issue_s(b, kslot);
-            mma_commit(bar_s_full(b));
+            commit(bar_s_full(b));
             FTRACE(2 + b, t);
           }
         }
-        mma_commit(bar_kv_empty(vslot));
+        commit(bar_kv_empty(vslot));
         if (more) {
-          mma_commit(bar_kv_empty(kslot));
+          commit(bar_kv_empty(kslot));
           if (++slot == STAGES) { slot = 0; phase ^= 1; }
         }
         FTRACE(15, t);
