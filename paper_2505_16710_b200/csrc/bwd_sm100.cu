@@ -38,6 +38,9 @@
 // mbarrier waits in this translation unit pass a suspend-time hint to try_wait: fewer polling
 // wavefronts on the shared-memory pipe, which the backward keeps ~90 % busy (+1.7-3 % per call;
 // the forward, compiled separately, measured -0.5 % with it and keeps the plain wait).
+#ifndef SECO_BWD_MMA_WARP
+#define SECO_BWD_MMA_WARP 1
+#endif
 #ifndef SECO_WAIT_HINT
 #define SECO_WAIT_HINT 1
 #endif
@@ -678,38 +681,51 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
       }
     } else if (warp == 1) {
       // -------------------------------------------------------------- MMA issuer
+#if SECO_BWD_MMA_WARP
+      // converged warp: every lane waits, one elected lane issues (operands stay warp-uniform)
+      const bool issuer = elect_one_sync();
+      {
+#else
+      const bool issuer = true;
       if (lane == 0) {
+#endif
         constexpr uint32_t idesc_s = make_idesc_bf16(BKV, BQ, 0, 0);
         constexpr uint32_t idesc_kv = make_idesc_bf16(BKV, D, 0, 1);
         constexpr uint32_t idesc_q = make_idesc_bf16(D, BQ, 1, 1);
+        // descriptors per tile base; a k-step adds its byte offset / 16 to the start-address field
         auto issue_sdp = [&](uint32_t a_base, uint32_t b_base, uint32_t d_col) {
+          const uint64_t da = make_desc_sw128(a_base, 16, 1024), db = make_desc_sw128(b_base, 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kBox + (kk % 4) * 32;
-            mma_ss(tmem + d_col, make_desc_sw128(a_base + off, 16, 1024), make_desc_sw128(b_base + off, 16, 1024),
-                   idesc_s, kk > 0);
+            const uint32_t off = ((kk / 4) * kBox + (kk % 4) * 32) >> 4;
+            if (issuer) mma_ss(tmem + d_col, da + off, db + off, idesc_s, kk > 0);
           }
         };
         // A = P^T / dS^T packed in TMEM (query k-step kk at columns base + 16 kk .. +7)
         auto issue_kv = [&](uint32_t a_col, uint32_t b_base, uint32_t d_col, bool acc) {
+          const uint64_t db = make_desc_sw128(b_base, kBox, 1024);
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tmem + d_col, tmem + a_col + 16 * kk, make_desc_sw128(b_base + kk * 2048, kBox, 1024), idesc_kv,
-                   (acc || kk > 0) ? 1u : 0u);
+            if (issuer)
+              mma_ts(tmem + d_col, tmem + a_col + 16 * kk, db + (uint32_t)(kk * 2048 >> 4), idesc_kv,
+                     (acc || kk > 0) ? 1u : 0u);
         };
+        auto commit = [&](uint32_t bar) { if (issuer) mma_commit(bar); };
+        const uint64_t dk_mn = make_desc_sw128(sK, kBox, 1024), dds_mn = make_desc_sw128(sDS, kBox, 1024);
+        const uint64_t dds_k = make_desc_sw128(sDS, 16, 1024);
         mbar_wait(bar_kv, 0);
         mbar_wait(bar_q_full(0), 0);
         tc_fence_after();
         issue_sdp(sK, qbuf(0), R0);                       // S^T(0)
-        mma_commit(bar_s_full);
+        commit(bar_s_full);
         mbar_wait(bar_do_full, 0);
         tc_fence_after();
         issue_sdp(sV, sDO, R1);                           // dP^T(0)
-        mma_commit(bar_dp_full);
+        commit(bar_dp_full);
         mbar_wait(bar_p_ready, 0);
         tc_fence_after();
         issue_kv(R0, sDO, TM_DV, false);                  // dV = P^T(0) dO(0)
-        mma_commit(bar_do_empty);
+        commit(bar_do_empty);
         for (int i = 0; i < n; ++i) {
           const int st = i & 1;
           const bool more = i + 1 < n;
@@ -717,7 +733,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
             mbar_wait(bar_q_full(st ^ 1), ((i + 1) >> 1) & 1);
             tc_fence_after();
             issue_sdp(sK, qbuf(st ^ 1), R0);
-            mma_commit(bar_s_full);
+            commit(bar_s_full);
             V2TRACE(2, i);
           }
           mbar_wait(bar_ds_ready, i & 1);
@@ -725,15 +741,18 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)           // dQ^T(i) = K^T dS^T(i) -> R1 (first: it
-            mma_ss(tmem + R1, make_desc_sw128(sK + kk * 2048, kBox, 1024),   // heads the serial chain)
-                   make_desc_sw128(sDS + kk * 2048, kBox, 1024), idesc_q, kk > 0);
-          mma_commit(bar_dq_full);
+            if (issuer)                                   // heads the serial chain)
+              mma_ss(tmem + R1, dk_mn + (uint32_t)(kk * 2048 >> 4), dds_mn + (uint32_t)(kk * 2048 >> 4), idesc_q,
+                     kk > 0);
+          commit(bar_dq_full);
           V2TRACE(4, i);
+          const uint64_t dq_mn = make_desc_sw128(qbuf(st), kBox, 1024);
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)            // dK(i) += dS^T(i) Q(i), A = dS^T from smem
-            mma_ss(tmem + TM_DK, make_desc_sw128(sDS + (kk / 4) * kBox + (kk % 4) * 32, 16, 1024),
-                   make_desc_sw128(qbuf(st) + kk * 2048, kBox, 1024), idesc_kv, (i > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(bar_q_empty(st));
+            if (issuer)
+              mma_ss(tmem + TM_DK, dds_k + (uint32_t)(((kk / 4) * kBox + (kk % 4) * 32) >> 4),
+                     dq_mn + (uint32_t)(kk * 2048 >> 4), idesc_kv, (i > 0 || kk > 0) ? 1u : 0u);
+          commit(bar_q_empty(st));
           if (more) {
             mbar_wait(bar_dq_empty, i & 1);               // dQ^T(i) drained from R1
             V2TRACE(5, i);
@@ -741,15 +760,15 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
             V2TRACE(6, i);
             tc_fence_after();
             issue_sdp(sV, sDO, R1);                       // dP^T(i+1)
-            mma_commit(bar_dp_full);
+            commit(bar_dp_full);
             mbar_wait(bar_p_ready, (i + 1) & 1);
             V2TRACE(7, i);
             tc_fence_after();
             issue_kv(R0, sDO, TM_DV, true);               // dV += P^T(i+1) dO(i+1)
-            mma_commit(bar_do_empty);
+            commit(bar_do_empty);
           }
         }
-        mma_commit(bar_acc);
+        commit(bar_acc);
       }
     } else if (warp == 3) {
       // -------------------------------------------------------------- dQ reduce issuer
