@@ -37,13 +37,13 @@ constexpr int BM = 128;  // query rows per tile (= UMMA M)
 constexpr int BN = 128;  // keys per K/V tile (= UMMA N of S, K of PV)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
 #ifndef SECO_FWD_EMU
-#define SECO_FWD_EMU 0
+#define SECO_FWD_EMU 2
 #endif
-constexpr int kEmuPairs = SECO_FWD_EMU;
+constexpr int kEmuPairs = SECO_FWD_EMU;     // of every 8 exponential pairs, this many use ex2_emu2
 #ifndef SECO_FWD_PDL
 #define SECO_FWD_PDL 1
 #endif
-constexpr int kSMs = 148;                  // B200    // of every 16 column pairs, this many use ex2_emu2
+constexpr int kSMs = 148;                  // B200
 #ifndef SECO_FWD_SPLIT
 #define SECO_FWD_SPLIT 3
 #endif
@@ -53,11 +53,8 @@ constexpr int kSMs = 148;                  // B200    // of every 16 column pair
 #ifndef SECO_FWD_MAXCH
 #define SECO_FWD_MAXCH 4
 #endif
-#ifndef SECO_FWD_EMU_MIDDLE
-#define SECO_FWD_EMU_MIDDLE 0
-#endif
 #ifndef SECO_FWD_PROD_SLEEP
-#define SECO_FWD_PROD_SLEEP 0
+#define SECO_FWD_PROD_SLEEP 200
 #endif
 #ifndef SECO_FWD_LSUM_AFTER
 #define SECO_FWD_LSUM_AFTER 1
@@ -363,12 +360,10 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           for (int i = 0; i < 32; i += 2) {
             const f2_t x = ffma2(f2u(v[cc * 32 + i], v[cc * 32 + i + 1]), sl2x2, negm);
             // EMU of the 16 pairs, evenly spread, run on the FMA pipe (ex2_emu2)
-#if SECO_FWD_EMU_MIDDLE
-            // FA4's placement: only the middle 32-key chunks, the last EMU of every 8 pairs
-            const bool emu = EMU > 0 && cc > 0 && cc < fwd::BN / 32 - 1 && (i / 2) % 8 >= 8 - EMU;
-#else
-            const bool emu = ((i / 2) * EMU) / 16 != ((i / 2 + 1) * EMU) / 16;
-#endif
+            // EMU of every 8 pairs, evenly spread, run on the FMA pipe (ex2_emu2); the MUFU unit
+            // then has slack beside the tensor pipe (2 of 8 measured best)
+            const int p8 = (i / 2) % 8;
+            const bool emu = (p8 * EMU) / 8 != ((p8 + 1) * EMU) / 8;
             const f2_t p2 = emu ? ex2_emu2(x) : f2(ex2(f2lo(x)), ex2(f2hi(x)));
 #if SECO_FWD_LSUM_AFTER
             v[cc * 32 + i] = (uint32_t)p2; v[cc * 32 + i + 1] = (uint32_t)(p2 >> 32);   // row sum after release
