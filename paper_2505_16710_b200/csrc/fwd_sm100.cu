@@ -47,6 +47,9 @@ constexpr int kSMs = 148;                  // B200
 #ifndef SECO_FWD_SPLIT
 #define SECO_FWD_SPLIT 3
 #endif
+#ifndef SECO_FWD_NAMED_P
+#define SECO_FWD_NAMED_P 1
+#endif
 #ifndef SECO_FWD_MMA_WARP
 #define SECO_FWD_MMA_WARP 1
 #endif
@@ -254,11 +257,19 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         const bool more = t + 1 < nT;
         for (int b = 0; b < NH; ++b) {
           if (b == 0) FTRACE(18, t);
+#if SECO_FWD_NAMED_P
+          named_bar_sync(1 + 2 * b, 128 + 32);
+#else
           mbar_wait(bar_p_half(b, 0), t & 1);
+#endif
           FTRACE(0 + b, t);
           tc_fence_after();
           issue_pv_half(b, vslot, 0, t > 0);
+#if SECO_FWD_NAMED_P
+          named_bar_sync(2 + 2 * b, 128 + 32);
+#else
           mbar_wait(bar_p_half(b, 1), t & 1);
+#endif
           FTRACE(11 + 3 * b, t);
           tc_fence_after();
           issue_pv_half(b, vslot, 1, true);
@@ -376,8 +387,12 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
         }
         tmem_wait_st();
         tc_fence_before();
+#if SECO_FWD_NAMED_P
+        named_bar_arrive(1 + 2 * b + hf, 128 + 32);   // the warpgroup's 128 threads + the MMA warp
+#else
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p_half(b, hf));
+#endif
         if (hf == 0 && lane == 0 && wq == 0) FTRACE(12 + b, t);
       };
 #pragma unroll
