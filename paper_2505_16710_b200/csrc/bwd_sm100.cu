@@ -262,36 +262,46 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       }
     } else if (warp == 1) {
       // -------------------------------------------------------------- MMA issuer
+#if SECO_BWD_MMA_WARP
+      const bool issuer = elect_one_sync();               // converged warp, one elected lane issues
+      {
+#else
+      const bool issuer = true;
       if (lane == 0) {
+#endif
         constexpr uint32_t idesc_s = make_idesc_bf16(BKV, BQ, 0, 0);    // S^T, dP^T
         constexpr uint32_t idesc_kv = make_idesc_bf16(BKV, D, 0, 1);    // dV, dK: A TMEM (K-major), B MN-major
         constexpr uint32_t idesc_q = make_idesc_bf16(D, BQ, 1, 1);      // dQ^T: A, B MN-major
         auto issue_sdp = [&](uint32_t a_base, uint32_t b_base, uint32_t d_col) {
+          const uint64_t da = make_desc_sw128(a_base, 16, 1024), db = make_desc_sw128(b_base, 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * kBox + (kk % 4) * 32;
-            mma_ss(tmem + d_col, make_desc_sw128(a_base + off, 16, 1024), make_desc_sw128(b_base + off, 16, 1024),
-                   idesc_s, kk > 0);
+            const uint32_t off = ((kk / 4) * kBox + (kk % 4) * 32) >> 4;
+            if (issuer) mma_ss(tmem + d_col, da + off, db + off, idesc_s, kk > 0);
           }
         };
         // A operand (P^T or dS^T, bf16 in TMEM): query k-step kk (queries 16kk..16kk+15) lives
         // packed in columns base + 16kk .. +7 (over the S^T / dP^T columns of those queries, which
         // their compute warp has already read); query half hf = k-steps 4hf .. 4hf+3
         auto issue_kv = [&](uint32_t a_col, uint32_t b_base, uint32_t d_col, int hf, bool acc) {
+          const uint64_t db = make_desc_sw128(b_base, kBox, 1024);
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int kk = 4 * hf + k4;
-            mma_ts(tmem + d_col, tmem + a_col + 16 * kk,
-                   make_desc_sw128(b_base + kk * 2048, kBox, 1024), idesc_kv, (acc || kk > 0) ? 1u : 0u);
+            if (issuer)
+              mma_ts(tmem + d_col, tmem + a_col + 16 * kk, db + (uint32_t)(kk * 2048 >> 4), idesc_kv,
+                     (acc || kk > 0) ? 1u : 0u);
           }
         };
+        auto commit = [&](uint32_t bar) { if (issuer) mma_commit(bar); };
+        const uint64_t dk_mn = make_desc_sw128(sK, kBox, 1024), dds_mn = make_desc_sw128(sDS, kBox, 1024);
         mbar_wait(bar_kv, 0);
         mbar_wait(bar_do_full(0), 0);
         mbar_wait(bar_q_full(0), 0);
         tc_fence_after();
         issue_sdp(sV, dobuf(0), R1);
         issue_sdp(sK, qbuf(0), R0);
-        mma_commit(bar_s_full);
+        commit(bar_s_full);
         for (int i = 0; i < n; ++i) {
           const int st = i & 1;
           // dV += P^T dO ; dK += dS^T Q, query half 0 while the compute warps finish half 1
@@ -304,14 +314,15 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           TRACE(16, i);
           tc_fence_after();
           issue_kv(R0, dobuf(st), TM_DV, 1, true);
-          mma_commit(bar_do_empty(st));
+          commit(bar_do_empty(st));
           issue_kv(R1, qbuf(st), TM_DK, 1, true);
-          mma_commit(bar_q_empty(st));
+          commit(bar_q_empty(st));
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)             // dQ^T = K^T dS^T -> R0
-            mma_ss(tmem + R0, make_desc_sw128(sK + kk * 2048, kBox, 1024),
-                   make_desc_sw128(sDS + kk * 2048, kBox, 1024), idesc_q, kk > 0);
-          mma_commit(bar_dq_full);
+            if (issuer)
+              mma_ss(tmem + R0, dk_mn + (uint32_t)(kk * 2048 >> 4), dds_mn + (uint32_t)(kk * 2048 >> 4), idesc_q,
+                     kk > 0);
+          commit(bar_dq_full);
           TRACE(2, i);
           if (i + 1 < n) {
             const int st1 = (i + 1) & 1;
@@ -325,11 +336,11 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
             mbar_wait(bar_q_full(st1), ph1);
             tc_fence_after();
             issue_sdp(sK, qbuf(st1), R0);                   // S^T(i+1) -> R0
-            mma_commit(bar_s_full);
+            commit(bar_s_full);
             TRACE(4, i);
           }
         }
-        mma_commit(bar_acc);
+        commit(bar_acc);
       }
     } else if (warp >= 4) {
       // -------------------------------------------------------------- compute warpgroups
