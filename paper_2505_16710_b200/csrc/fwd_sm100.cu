@@ -40,6 +40,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when th
 #define SECO_FWD_EMU 2
 #endif
 constexpr int kEmuPairs = SECO_FWD_EMU;     // of every 8 exponential pairs, this many use ex2_emu2
+#ifndef SECO_FWD_EMU2
+#define SECO_FWD_EMU2 0
+#endif
+constexpr int kEmuPairs2 = SECO_FWD_EMU2;   // the same for the part released second (MUFU only)
 #ifndef SECO_FWD_PDL
 #define SECO_FWD_PDL 1
 #endif
@@ -398,7 +402,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         if (diag) exp_half(hf, std::integral_constant<int, 0>{});
-        else exp_half(hf, std::integral_constant<int, fwd::kEmuPairs>{});
+        else if (hf == 0) exp_half(hf, std::integral_constant<int, fwd::kEmuPairs>{});
+        else exp_half(hf, std::integral_constant<int, fwd::kEmuPairs2>{});
       }
       if (lane == 0 && wq == 0) FTRACE(8 + b, t);
 #if SECO_FWD_LSUM_AFTER
