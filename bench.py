@@ -518,7 +518,9 @@ def main():
                                    deterministic=args.deterministic, layout="shd") for _ in range(2)]
         out_dq = [torch.empty(seq, hq_r, d, dtype=tdt).pin_memory() for _ in range(2)]
         out_dkv = [torch.empty(layers[0].dkv.shape, dtype=layers[0].dkv.dtype).pin_memory() for _ in range(2)]
-        h2d = sum(t.numel() * t.element_size() for t in host)
+        need_do = {op[1] for op in order if op[0] == "b"}      # chunks whose backward reads dO_j
+        h2d = sum(t.numel() * t.element_size() for t in host[:3]) + \
+            host[3].numel() * host[3].element_size() * len(need_do) // k
         d2h = out_dq[0].numel() * out_dq[0].element_size() + out_dkv[0].numel() * out_dkv[0].element_size()
         s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         done = [None, None]      # compute-finished event of the last step that used set b
@@ -554,8 +556,9 @@ def main():
                         for dst, src in ((kd, host[1]), (vd, host[2]), (qd, host[0])):
                             rows(dst, j).copy_(rows(src, j), non_blocking=True)
                         ev_qkv[j].record(s_in)
-                    for j in reversed(range(k)):             # stage-2 order
-                        rows(dod, j).copy_(rows(host[3], j), non_blocking=True)
+                    for j in reversed(range(k)):             # stage-2 order; SpaCO: sampled chunks
+                        if j in need_do:                     # only (a skipped chunk's dO is never read)
+                            rows(dod, j).copy_(rows(host[3], j), non_blocking=True)
                         ev_do[j].record(s_in)
                 if drained[b] is not None:
                     stream.wait_event(drained[b])
@@ -610,7 +613,8 @@ def main():
                "ms_per_step": ems / args.steps, "ms_per_step_median": statistics.median(e2e_per_step),
                "ms_per_step_min": min(e2e_per_step), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "pinned host Q,K,V,dO ([S][h][d]) -> device per chunk in the order the step consumes "
-                       "them (copy stream); SeCO/SpaCO chunk calls via the C ABI, each waiting only for its "
+                       "them (copy stream; SpaCO: dO only for the sampled chunks); SeCO/SpaCO chunk calls via the C "
+                       "ABI, each waiting only for its "
                        "chunk's inputs; dQ_j, dKV slot j -> pinned host as soon as chunk j's backward (or "
                        "skip) is done (copy stream, dKV slot as one 2-D copy); steps double-buffered; W untimed "
                        "warm-up steps of the same pipeline first; per-step times = intervals between "
