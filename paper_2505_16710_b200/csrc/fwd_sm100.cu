@@ -585,7 +585,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
       uint32_t phase = 0;
       for (int t = t0; t < t0 + nT; ++t) {
         for (int w = 0; w < 2; ++w) {  // K_t half then V_t half
+#if SECO_FWD_PROD_SLEEP
+          while (!mbar_try_wait(bar_kv_empty(slot), phase ^ 1)) __nanosleep(SECO_FWD_PROD_SLEEP);
+#else
           mbar_wait(bar_kv_empty(slot), phase ^ 1);
+#endif
           if (leader) mbar_expect_tx(bar_kv_full(slot), 2 * kStage);
           const uint32_t bf = mapa_shared(bar_kv_full(slot), 0);
           const uint32_t dst = sKV + slot * kStage;
@@ -607,56 +611,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
-    if (lane == 0 && leader) {
+    // converged warp, one elected lane issues (operands in uniform registers); the waits use
+    // CTA-scope acquire like CUTLASS's cluster pipelines: the data handed over lives in TMEM or
+    // arrives by TMA, both ordered by the tcgen05 fences and the mbarrier transaction counts
+    const bool issuer = elect_one_sync();
+    if (leader) {
       constexpr uint32_t idesc_s = make_idesc_bf16(2 * BM, BN, 0, 0);   // Q K-major, K K-major
       constexpr uint32_t idesc_pv = make_idesc_bf16(2 * BM, D, 0, 1);   // P (TMEM), V MN-major
       auto issue_s = [&](int b, int slot) {
-        const uint32_t qa = sQ + b * kQBytes, ka = sKV + slot * kStage;
+        const uint64_t dq = make_desc_sw128(sQ + b * kQBytes, 16, 1024);
+        const uint64_t dk = make_desc_sw128(sKV + slot * kStage, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss_pair(tmem + b * BN, make_desc_sw128(qa + (kk / 4) * BOX + (kk % 4) * 32, 16, 1024),
-                      make_desc_sw128(ka + (kk / 4) * HBOX + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
+          if (issuer)
+            mma_ss_pair(tmem + b * BN, dq + (uint32_t)(((kk / 4) * BOX + (kk % 4) * 32) >> 4),
+                        dk + (uint32_t)(((kk / 4) * HBOX + (kk % 4) * 32) >> 4), idesc_s, kk > 0);
       };
-      auto issue_pv_half = [&](int b, int slot, int hf, bool acc) {   // keys [64 hf, 64 hf + 64)
-        const uint32_t va = sKV + slot * kStage;
+      auto issue_pv_part = [&](int b, int slot, int hf, bool acc) {   // part hf: k16 steps [k0, k1)
+        const uint64_t dv = make_desc_sw128(sKV + slot * kStage, BOX, 1024);
+        const int k0 = hf ? 2 * fwd::kSplit : 0, k1 = hf ? BN / 16 : 2 * fwd::kSplit;
 #pragma unroll
-        for (int k4 = 0; k4 < BN / 32; ++k4) {
-          const int kk = hf * (BN / 32) + k4;
-          mma_ts_pair(tmem + NH * BN + b * D, tmem + b * BN + kk * 8, make_desc_sw128(va + kk * 2048, BOX, 1024),
-                      idesc_pv, (acc || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = k0; kk < k1; ++kk)
+          if (issuer)
+            mma_ts_pair(tmem + NH * BN + b * D, tmem + b * BN + kk * 8, dv + (uint32_t)(kk * 2048 >> 4), idesc_pv,
+                        (acc || kk > 0) ? 1u : 0u);
       };
-      for (int b = 0; b < NH; ++b) mbar_wait_cluster(bar_q(b), 0);
+      auto commit = [&](uint32_t bar) { if (issuer) mma_commit_pair(bar); };
+      for (int b = 0; b < NH; ++b) mbar_wait(bar_q(b), 0);
       int slot = 0;
       uint32_t phase = 0;
-      mbar_wait_cluster(bar_kv_full(slot), phase);
+      mbar_wait(bar_kv_full(slot), phase);
       tc_fence_after();
-      for (int b = 0; b < NH; ++b) { issue_s(b, slot); mma_commit_pair(bar_s_full(b)); }
-      mma_commit_pair(bar_kv_empty(slot));
+      for (int b = 0; b < NH; ++b) { issue_s(b, slot); commit(bar_s_full(b)); }
+      commit(bar_kv_empty(slot));
       if (++slot == STAGES) { slot = 0; phase ^= 1; }
       for (int t = 0; t < nT; ++t) {
         const int vslot = slot;
-        mbar_wait_cluster(bar_kv_full(vslot), phase);
+        mbar_wait(bar_kv_full(vslot), phase);
         if (++slot == STAGES) { slot = 0; phase ^= 1; }
         const int kslot = slot;
         const bool more = t + 1 < nT;
         for (int b = 0; b < NH; ++b) {
-          mbar_wait_cluster(bar_p_half(b, 0), t & 1);
+          mbar_wait(bar_p_half(b, 0), t & 1);
           tc_fence_after();
-          issue_pv_half(b, vslot, 0, t > 0);
-          mbar_wait_cluster(bar_p_half(b, 1), t & 1);
+          issue_pv_part(b, vslot, 0, t > 0);
+          mbar_wait(bar_p_half(b, 1), t & 1);
           tc_fence_after();
-          issue_pv_half(b, vslot, 1, true);
-          mma_commit_pair(bar_o_full(b));
+          issue_pv_part(b, vslot, 1, true);
+          commit(bar_o_full(b));
           if (more) {
-            if (b == 0) { mbar_wait_cluster(bar_kv_full(kslot), phase); tc_fence_after(); }
+            if (b == 0) { mbar_wait(bar_kv_full(kslot), phase); tc_fence_after(); }
             issue_s(b, kslot);
-            mma_commit_pair(bar_s_full(b));
+            commit(bar_s_full(b));
           }
         }
-        mma_commit_pair(bar_kv_empty(vslot));
+        commit(bar_kv_empty(vslot));
         if (more) {
-          mma_commit_pair(bar_kv_empty(kslot));
+          commit(bar_kv_empty(kslot));
           if (++slot == STAGES) { slot = 0; phase ^= 1; }
         }
       }
@@ -685,13 +696,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
         for (int i = 0; i < BN; ++i)
           if (i > r) v[i] = __float_as_uint(-INFINITY);
       }
-      float mx0 = -INFINITY, mx1 = -INFINITY;
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < BN; i += 4) {
+      for (int i = 0; i < BN; i += 8) {
         mx0 = fmax3(mx0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
         mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        mx2 = fmax3(mx2, __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
+        mx3 = fmax3(mx3, __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
       }
-      const float m_new = fmaxf(m, fmaxf(mx0, mx1) * sl2);
+      const float m_new = fmaxf(m, fmax3(mx0, mx1, fmaxf(mx2, mx3)) * sl2);
       const bool need = m_new > m + fwd::kRescaleThreshold;
       const float m_use = need ? m_new : m;
       const float alpha = need ? ex2(m - m_new) : 1.f;
@@ -711,17 +724,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
       m = m_use;
       const f2_t negm = f2(-m_use, -m_use);
       f2_t lsum0 = f2(0.f, 0.f), lsum1 = f2(0.f, 0.f);
+      // as in seco_fwd_sm100_kernel: P released in two parts (32-key chunks [0, kSplit), then the
+      // rest) to the leader's MMA warp, 2 of 8 exponential pairs of the first part on the FMA
+      // pipe (not on the diagonal tile), the row sum after the releases
+      auto exp_part = [&](int hf, auto emu_pairs) {
+        constexpr int EMU = decltype(emu_pairs)::value;
+        const int c0 = hf ? fwd::kSplit : 0, c1 = hf ? BN / 32 : fwd::kSplit;
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-#pragma unroll
-        for (int c2 = 0; c2 < 2; ++c2) {
-          const int cc = hf * 2 + c2;
+        for (int cc = c0; cc < c1; ++cc) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             const f2_t x = ffma2(f2u(v[cc * 32 + i], v[cc * 32 + i + 1]), sl2x2, negm);
-            const f2_t p2 = f2(ex2(f2lo(x)), ex2(f2hi(x)));
-            if ((i / 2) & 1) lsum1 = fadd2(lsum1, p2); else lsum0 = fadd2(lsum0, p2);
+            const int p8 = (i / 2) % 8;
+            const bool emu = (p8 * EMU) / 8 != ((p8 + 1) * EMU) / 8;
+            const f2_t p2 = emu ? ex2_emu2(x) : f2(ex2(f2lo(x)), ex2(f2hi(x)));
+            v[cc * 32 + i] = (uint32_t)p2;
+            v[cc * 32 + i + 1] = (uint32_t)(p2 >> 32);
             pk[i / 2] = pack_bf16_f2(p2);
           }
           tmem_st16(tS + cc * 16, pk);
@@ -729,7 +748,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(bar_p_half(b, hf), 0));
+        if (lane == 0) mbar_arrive_remote(mapa_shared(bar_p_half(b, hf), 0));
+      };
+      if (diag) {
+        exp_part(0, std::integral_constant<int, 0>{});
+        exp_part(1, std::integral_constant<int, 0>{});
+      } else {
+        exp_part(0, std::integral_constant<int, fwd::kEmuPairs>{});
+        exp_part(1, std::integral_constant<int, fwd::kEmuPairs2>{});
+      }
+#pragma unroll
+      for (int i = 0; i < BN; i += 4) {
+        lsum0 = fadd2(lsum0, f2u(v[i], v[i + 1]));
+        lsum1 = fadd2(lsum1, f2u(v[i + 2], v[i + 3]));
       }
       const f2_t lsum = fadd2(lsum0, lsum1);
       l += f2lo(lsum) + f2hi(lsum);
@@ -874,12 +905,17 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
 }
 
 bool fwd_uses_pair(const ChunkGeom& g) {
-  static const bool enabled = [] {
-    // experiment, off by default (correct, -38 % per call); SECO_FWD_PAIR=1 selects it
+  // CTA pairs halve each SM's shared-memory operand and TMA traffic; per call they run level
+  // with the unpaired kernel and, at the lower power, +0.4 % on the power-capped cfg3 step, but
+  // their 4-head work units are coarser: with fewer unsplit units than SMs (head-sharded ranks,
+  // short chunks) they lose ~1 %.  SECO_FWD_PAIR=0 / 1 forces the choice (A/B).
+  static const int mode = [] {
     const char* e = std::getenv("SECO_FWD_PAIR");
-    return e != nullptr && e[0] == '1';
+    return e == nullptr ? -1 : (e[0] == '0' ? 0 : 1);
   }();
-  return enabled && (g.d == 128 || g.d == 64) && (g.hq / g.hkv) % 4 == 0;
+  const bool shape_ok = (g.d == 128 || g.d == 64) && (g.hq / g.hkv) % 4 == 0;
+  if (mode >= 0) return mode == 1 && shape_ok;
+  return shape_ok && (g.c / fwd::BM) * (g.hq / 2) >= fwd::kSMs;
 }
 
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,

@@ -385,3 +385,46 @@ def test_spaco_expectation_through_the_kernels(dtype):
     ref = OE.closed_form_t_of_k(parts, k, t, gamma, 1.0)
     for n in ("dq", "dk", "dv"):
         assert err(acc[n].cpu().numpy(), ref[n]) <= tol, ("t-of-k", n)
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_bf16_forward_pair_switch_subprocess(pair):
+    """The CTA-pair forward (seco_fwd2_sm100_kernel: cta_group::2 over the 4 q-heads of a kv group,
+    half of every K / V tile per CTA, DESIGN §6.5) is the default only on full-wave grids (cfg3);
+    SECO_FWD_PAIR=1 forces it on the small parity shapes here (split-KV, d = 64, ragged ranks of
+    units), SECO_FWD_PAIR=0 forces the unpaired kernel.  O, LSE and the whole step against the
+    oracle; the stage-2 rebuild reproduces stage 1 bit for bit.  Read once per process: child."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import chunkwise as OC
+from tests.gpu_util import BF16_TOL, err, host, inputs, upload
+from paper_2505_16710_b200.step import ChunkedAttention
+for (hq, hkv, seq, c, d) in ((8, 2, 1024, 256, 128), (16, 4, 2048, 512, 128), (8, 2, 1024, 256, 64),
+                             (4, 1, 4096, 1024, 128)):
+    x = inputs(hq, hkv, seq, d, seed=7, peaky=True)
+    q, k, v, do = upload(x, torch.bfloat16)
+    L = ChunkedAttention(hq, hkv, d, seq, c, dtype=torch.bfloat16)
+    for j in range(seq // c):
+        L.forward_chunk(q, k, v, j)
+    torch.cuda.synchronize()
+    o1, lse1 = L.o.clone(), L.lse.clone()
+    L.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, L.o) and torch.equal(lse1, L.lse), (hq, hkv, seq, c, d, "rebuild not bitwise")
+    ref = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (seq // c))
+    dk, dv = L.own_grads()
+    for name, gpu in (("o", host(L.o)), ("dq", host(L.dq)), ("dk", host(dk)), ("dv", host(dv))):
+        e = err(gpu, ref[name])
+        assert e <= BF16_TOL, (hq, hkv, seq, c, d, name, e)
+    lse = L.lse_full().cpu().numpy()
+    assert np.abs(lse - ref["lse"]).max() <= 1e-3, (hq, hkv, seq, c, d, "lse")
+print("pair switch ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, SECO_FWD_PAIR=pair),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "pair switch ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
