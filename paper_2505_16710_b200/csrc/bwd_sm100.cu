@@ -38,6 +38,9 @@
 // mbarrier waits in this translation unit pass a suspend-time hint to try_wait: fewer polling
 // wavefronts on the shared-memory pipe, which the backward keeps ~90 % busy (+1.7-3 % per call;
 // the forward, compiled separately, measured -0.5 % with it and keeps the plain wait).
+#ifndef SECO_BWD_PAIR_DEFAULT
+#define SECO_BWD_PAIR_DEFAULT 0
+#endif
 #ifndef SECO_BWD_MMA_WARP
 #define SECO_BWD_MMA_WARP 1
 #endif
@@ -986,6 +989,465 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ============================================================================ backward v3 (CTA pairs)
+// seco_bwd3_sm100_kernel: the v2 algorithm (same MMAs, issue order, TMEM regions, drain and compute
+// warps) on clusters of 2 CTAs = two adjacent key tiles (2u, 2u + 1) of one kv head that walk the
+// same query tiles.  Four of the five MMAs per block run as tcgen05.mma.cta_group::2 with M = 256
+// (each CTA's 128 keys), issued by the leader:
+//   S^T  = K Q^T    B = Q^T: each CTA holds its 64 query rows of Q(i) (Qr)
+//   dP^T = V dO^T   B = dO^T: its 64 query rows of dO(i) (dOr)
+//   dV  += P^T dO   B = dO: its 64 d columns of dO(i), every query row (dOc)
+//   dK  += dS^T Q   B = Q: its 64 d columns of Q(i) (Qc)
+// so each SM reads half of every B operand from shared memory; dQ^T = K^T dS^T contracts over the
+// keys and stays per CTA (cta_group::1, issued by each CTA's own MMA warp).  Hand-offs to the
+// leader's MMA warp (both CTAs' P^T ready, dS^T ready, dQ^T drained) are remote mbarrier arrives
+// with CTA-scope semantics (TMEM / smem data ordered by the tcgen05 fences and the proxy fence);
+// the leader's commits reach both CTAs by multicast.  DESIGN §6.2.
+namespace bwd3 {
+constexpr int BKV = 128, BQ = 128, D = 128;
+constexpr int kTile = 128 * 128 * 2;           // bf16 [128][128]
+constexpr int kBox = 128 * 128;                // one [128 rows][128 B] box
+constexpr int kHalf = 64 * 128;                // one [64 rows][128 B] box
+constexpr int kK = 0;
+constexpr int kV = kK + kTile;
+constexpr int kQ = kV + kTile;                 // two stages of {Qr: 2 x [64][64], Qc: [128][64]}
+constexpr int kQStage = 2 * kHalf + kBox;      // 32 KiB
+constexpr int kDO = kQ + 2 * kQStage;          // one stage of {dOr, dOc}
+constexpr int kSTG = kDO + kQStage;            // dQ staging: 2 slots x 16 KiB
+constexpr int kSlot = 32 * D * 4;
+constexpr int kDS = kSTG + 2 * kSlot;          // dS^T [128 keys][128 q] bf16 (2 boxes by q half)
+constexpr int kStats = kDS + kTile;            // [2 stages][2][BQ] fp32 (-LSE log2e, D)
+constexpr int kBar = kStats + 2 * 2 * BQ * 4;
+constexpr int kNumBars = 24;
+constexpr int kTmemSlot = kBar + 8 * kNumBars;
+constexpr int kBytes = kTmemSlot + 16;
+constexpr int kThreads = 512;
+constexpr int R0 = 0, R1 = 128, TM_DK = 256, TM_DV = 384;
+}  // namespace bwd3
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(bwd3::kThreads, 1)
+    seco_bwd3_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                           const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_do64,
+                           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                           const __grid_constant__ CUtensorMap tm_dkv, const bwd::Args a) {
+  using namespace bwd3;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t sK = sb + kK, sV = sb + kV, sDO = sb + kDO, sDS = sb + kDS, sSTG = sb + kSTG;
+  auto qbuf = [&](int st) { return sb + kQ + (uint32_t)st * kQStage; };   // Qr at +0, Qc at +2 kHalf
+  const uint32_t sStats = sb + kStats;
+  const uint32_t b0 = sb + kBar;
+  const uint32_t bar_kv = b0;
+  auto bar_q_full = [&](int s) { return b0 + 8u * (1 + s); };      // leader: both CTAs' Q halves
+  auto bar_q_empty = [&](int s) { return b0 + 8u * (3 + s); };     // local, multicast release
+  const uint32_t bar_do_full = b0 + 8u * 5, bar_do_empty = b0 + 8u * 6;
+  const uint32_t bar_s_full = b0 + 8u * 7;                          // local, multicast commit
+  const uint32_t bar_p_ready = b0 + 8u * 8;                         // leader: 16 compute warps
+  const uint32_t bar_dp_full = b0 + 8u * 9;                         // local, multicast commit
+  const uint32_t bar_ds_ready = b0 + 8u * 10;                       // local: own dQ^T
+  const uint32_t bar_dq_full = b0 + 8u * 11;                        // local: own dQ^T done
+  const uint32_t bar_dq_empty = b0 + 8u * 12;                       // leader: 8 drain warps
+  auto bar_stg_full = [&](int s) { return b0 + 8u * (13 + s); };
+  auto bar_stg_free = [&](int s) { return b0 + 8u * (15 + s); };
+  const uint32_t bar_acc = b0 + 8u * 17, bar_drain_done = b0 + 8u * 18;
+  const uint32_t bar_ds_pair = b0 + 8u * 19;                        // leader: 16 compute warps
+  auto bar_st_full = [&](int s) { return b0 + 8u * (20 + s); };    // local: this CTA's stats
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kTmemSlot);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int rank = (int)cluster_ctarank();
+  const bool leader = rank == 0;
+  constexpr uint16_t kPair = 3;
+
+  // work decode over pair units (clusters = blockIdx / 2); the pair walks its first tile's queries
+  const int bid = (int)blockIdx.x >> 1;
+  int U, piece, f;
+  if (bid < a.n0) {
+    U = bid; piece = 0; f = 1;
+  } else if (bid < a.n0 + a.n1 * a.f1) {
+    const int r = bid - a.n0;
+    U = a.n0 + r / a.f1; piece = r % a.f1; f = a.f1;
+  } else {
+    const int r = bid - a.n0 - a.n1 * a.f1;
+    U = a.n0 + a.n1 + r / a.f2; piece = r % a.f2; f = a.f2;
+  }
+  const int g = U % a.hkv;
+  const int u = 2 * (U / a.hkv) + rank;
+  const int k0 = u * BKV;
+  const int nqt = a.c / BQ;
+  const int rel = 2 * (U / a.hkv) * BKV - a.j * a.c;
+  const int qt_min = rel > 0 ? rel / BQ : 0;
+  const int n_all = a.G * (nqt - qt_min);
+  const int it0 = (int)((int64_t)piece * n_all / f);
+  const int it1 = (int)((int64_t)(piece + 1) * n_all / f);
+  const int n = it1 - it0;
+  struct Walk {
+    int hh, qt, G;
+    __device__ void next() { if (++hh == G) { hh = 0; ++qt; } }
+  };
+  const Walk walk0{it0 % a.G, qt_min + it0 / a.G, a.G};
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_kv, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar_q_full(s), 1);
+      mbar_init(bar_q_empty(s), 1);
+      mbar_init(bar_stg_full(s), 4);    // the 4 drain warps
+      mbar_init(bar_stg_free(s), 1);
+      mbar_init(bar_st_full(s), 1);
+    }
+    mbar_init(bar_do_full, 1);
+    mbar_init(bar_do_empty, 1);
+    mbar_init(bar_s_full, 1);
+    mbar_init(bar_p_ready, 16);         // 8 compute warps x 2 CTAs (leader's copy)
+    mbar_init(bar_dp_full, 1);
+    mbar_init(bar_ds_ready, 8);         // this CTA's 8 compute warps
+    mbar_init(bar_ds_pair, 16);
+    mbar_init(bar_dq_full, 1);
+    mbar_init(bar_dq_empty, 8);         // 4 drain warps x 2 CTAs (leader's copy)
+    mbar_init(bar_acc, 1);
+    mbar_init(bar_drain_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_q); tma_prefetch(&tm_do); tma_prefetch(&tm_q64); tma_prefetch(&tm_do64);
+    tma_prefetch(&tm_k); tma_prefetch(&tm_v); tma_prefetch(&tm_dkv);
+  }
+  if (warp == 2) tmem_alloc_pair<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                      // both CTAs' barriers initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (n > 0) {
+    if (warp == 0) {
+      // -------------------------------------------------------------- TMA producer (both CTAs)
+      if (lane == 0) {
+        mbar_expect_tx(bar_kv, 2 * kTile);
+        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && g < a.hkv, 413);
+        for (int x = 0; x < D / 64; ++x) {
+          tma_load_3d(sK + x * kBox, &tm_k, bar_kv, x * 64, k0, g);
+          tma_load_3d(sV + x * kBox, &tm_v, bar_kv, x * 64, k0, g);
+        }
+        Walk w = walk0;
+        for (int i = 0; i < n; ++i, w.next()) {
+          const int st = i & 1;
+          const uint32_t ph = (i >> 1) & 1;
+          const int h = g * a.G + w.hh, qt = w.qt;
+          SECO_CHECK_COND(qt * BQ + BQ <= a.c && w.hh < a.G, 414);
+          mbar_wait(bar_q_empty(st), ph ^ 1);
+          if (leader) mbar_expect_tx(bar_q_full(st), 2 * kQStage);
+          const uint32_t bq = mapa_shared(bar_q_full(st), 0);
+          for (int x = 0; x < D / 64; ++x)      // Qr: this CTA's 64 query rows, all d
+            tma_load_3d_pair(qbuf(st) + x * kHalf, &tm_q64, bq, x * 64, qt * BQ + 64 * rank, h, kHalf);
+          tma_load_3d_pair(qbuf(st) + 2 * kHalf, &tm_q, bq, 64 * rank, qt * BQ, h, kBox);   // Qc
+          const int64_t ro = (int64_t)h * a.c + qt * BQ;
+          mbar_expect_tx(bar_st_full(st), 2 * BQ * 4);
+          bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_st_full(st));
+          bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_st_full(st));
+          mbar_wait(bar_do_empty, (i & 1) ^ 1);
+          if (leader) mbar_expect_tx(bar_do_full, 2 * kQStage);
+          const uint32_t bdo = mapa_shared(bar_do_full, 0);
+          for (int x = 0; x < D / 64; ++x)
+            tma_load_3d_pair(sDO + x * kHalf, &tm_do64, bdo, x * 64, qt * BQ + 64 * rank, h, kHalf);
+          tma_load_3d_pair(sDO + 2 * kHalf, &tm_do, bdo, 64 * rank, qt * BQ, h, kBox);
+        }
+        // the leader's last multicast releases have landed in this CTA before the pair may exit
+        for (int i = n; i < n + 2; ++i) mbar_wait(bar_q_empty(i & 1), ((i >> 1) & 1) ^ 1);
+        mbar_wait(bar_do_empty, (n & 1) ^ 1);
+      }
+    } else if (warp == 1) {
+      // -------------------------------------------------------------- MMA issuer
+      // converged warp, one elected lane issues.  Leader: the pair's S^T, dP^T, dV, dK (M = 256)
+      // and its own dQ^T; follower: its own dQ^T only.
+      const bool issuer = elect_one_sync();
+      constexpr uint32_t idesc_s = make_idesc_bf16(2 * BKV, BQ, 0, 0);
+      constexpr uint32_t idesc_kv = make_idesc_bf16(2 * BKV, D, 0, 1);
+      constexpr uint32_t idesc_q = make_idesc_bf16(D, BQ, 1, 1);
+      const uint64_t dk_mn = make_desc_sw128(sK, kBox, 1024), dds_mn = make_desc_sw128(sDS, kBox, 1024);
+      auto issue_dq = [&]() {                          // dQ^T = K^T dS^T -> R1 (this CTA)
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          if (issuer)
+            mma_ss(tmem + R1, dk_mn + (uint32_t)(kk * 2048 >> 4), dds_mn + (uint32_t)(kk * 2048 >> 4), idesc_q,
+                   kk > 0);
+        if (issuer) mma_commit(bar_dq_full);
+      };
+      if (!leader) {
+        for (int i = 0; i < n; ++i) {
+          mbar_wait(bar_ds_ready, i & 1);
+          tc_fence_after();
+          issue_dq();
+        }
+      } else {
+        // A = K / V (this CTA's 128 keys, K-major boxes of 128 rows); B = the 64-row halves
+        auto issue_sdp = [&](uint32_t a_base, uint32_t b_base, uint32_t d_col) {
+          const uint64_t da = make_desc_sw128(a_base, 16, 1024), db = make_desc_sw128(b_base, 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            if (issuer)
+              mma_ss_pair(tmem + d_col, da + (uint32_t)(((kk / 4) * kBox + (kk % 4) * 32) >> 4),
+                          db + (uint32_t)(((kk / 4) * kHalf + (kk % 4) * 32) >> 4), idesc_s, kk > 0);
+        };
+        // A = P^T (TMEM, packed bf16); B = the d-column half (one [128 q][64 d] box, MN-major)
+        auto issue_kv = [&](uint32_t a_col, uint32_t b_base, uint32_t d_col, bool acc) {
+          const uint64_t db = make_desc_sw128(b_base, kBox, 1024);
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            if (issuer)
+              mma_ts_pair(tmem + d_col, tmem + a_col + 16 * kk, db + (uint32_t)(kk * 2048 >> 4), idesc_kv,
+                          (acc || kk > 0) ? 1u : 0u);
+        };
+        auto commit2 = [&](uint32_t bar) { if (issuer) mma_commit_pair(bar); };
+        const uint64_t dds_k = make_desc_sw128(sDS, 16, 1024);
+        mbar_wait(bar_kv, 0);
+        mbar_wait(bar_q_full(0), 0);
+        tc_fence_after();
+        issue_sdp(sK, qbuf(0), R0);                       // S^T(0)
+        commit2(bar_s_full);
+        mbar_wait(bar_do_full, 0);
+        tc_fence_after();
+        issue_sdp(sV, sDO, R1);                           // dP^T(0)
+        commit2(bar_dp_full);
+        mbar_wait(bar_p_ready, 0);
+        tc_fence_after();
+        issue_kv(R0, sDO + 2 * kHalf, TM_DV, false);      // dV = P^T(0) dO(0)
+        commit2(bar_do_empty);
+        for (int i = 0; i < n; ++i) {
+          const int st = i & 1;
+          const bool more = i + 1 < n;
+          if (more) {                                     // S^T(i+1) -> R0 (P^T(i) consumed by dV(i))
+            mbar_wait(bar_q_full(st ^ 1), ((i + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_sdp(sK, qbuf(st ^ 1), R0);
+            commit2(bar_s_full);
+          }
+          mbar_wait(bar_ds_ready, i & 1);                 // own dS^T(i): own dQ^T first (heads the chain)
+          tc_fence_after();
+          issue_dq();
+          mbar_wait(bar_ds_pair, i & 1);                  // both CTAs' dS^T(i)
+          tc_fence_after();
+          const uint64_t dq_mn = make_desc_sw128(qbuf(st) + 2 * kHalf, kBox, 1024);
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk)            // dK(i) += dS^T(i) Q(i) (pair)
+            if (issuer)
+              mma_ss_pair(tmem + TM_DK, dds_k + (uint32_t)(((kk / 4) * kBox + (kk % 4) * 32) >> 4),
+                          dq_mn + (uint32_t)(kk * 2048 >> 4), idesc_kv, (i > 0 || kk > 0) ? 1u : 0u);
+          commit2(bar_q_empty(st));
+          if (more) {
+            mbar_wait(bar_dq_empty, i & 1);               // both CTAs' dQ^T(i) drained from R1
+            mbar_wait(bar_do_full, (i + 1) & 1);
+            tc_fence_after();
+            issue_sdp(sV, sDO, R1);                       // dP^T(i+1)
+            commit2(bar_dp_full);
+            mbar_wait(bar_p_ready, (i + 1) & 1);
+            tc_fence_after();
+            issue_kv(R0, sDO + 2 * kHalf, TM_DV, true);   // dV += P^T(i+1) dO(i+1)
+            commit2(bar_do_empty);
+          }
+        }
+        commit2(bar_acc);
+      }
+    } else if (warp == 3) {
+      // -------------------------------------------------------------- dQ reduce issuer
+      if (lane == 0) {
+        Walk w = walk0;
+        int m = 0;
+        for (int i = 0; i < n; ++i, w.next()) {
+          const int h = g * a.G + w.hh, qt = w.qt;
+          float* dst = a.dqacc + ((int64_t)h * a.c + qt * BQ) * D;
+          for (int c = 0; c < 4; ++c, ++m) {
+            const int s = c & 1;
+            mbar_wait(bar_stg_full(s), (m >> 1) & 1);
+            SECO_CHECK_COND(dst >= a.dqacc && dst + 32 * (c + 1) * D <= a.dqacc + (int64_t)a.G * a.hkv * a.c * D, 513);
+            bulk_reduce_add_f32(dst + 32 * c * D, sSTG + s * kSlot, kSlot);
+            bulk_commit();
+            if (m > 0) {
+              bulk_wait_read<1>();
+              mbar_arrive(bar_stg_free(s ^ 1));
+            }
+          }
+        }
+        bulk_wait_read<0>();
+        mbar_arrive(bar_stg_free((m - 1) & 1));
+        bulk_wait0();
+        mbar_arrive(bar_drain_done);
+      }
+    } else if (warp >= 4 && warp < 8) {
+      // -------------------------------------------------------------- dQ^T drain (lane = d)
+      const int wq = warp % 4;
+      const int dr = wq * 32 + lane;
+      const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+      const uint32_t dq_empty_l = mapa_shared(bar_dq_empty, 0);
+      int m = 0;
+      auto stage = [&](const uint32_t (&v)[32], int s) {
+        mbar_wait(bar_stg_free(s), ((m >> 1) & 1) ^ 1);
+        const uint32_t base = sSTG + s * kSlot + dr * 4;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) st_shared_f32(base + q * (D * 4), __uint_as_float(v[q]));
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_stg_full(s));
+        ++m;
+      };
+      for (int i = 0; i < n; ++i) {
+        mbar_wait(bar_dq_full, i & 1);
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld32(tmem + lane_addr + R1, v0);
+        tmem_wait_ld();
+        stage(v0, 0);
+        tmem_ld32(tmem + lane_addr + R1 + 32, v1);
+        tmem_wait_ld();
+        stage(v1, 1);
+        tmem_ld32(tmem + lane_addr + R1 + 64, v0);
+        tmem_ld32(tmem + lane_addr + R1 + 96, v1);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(dq_empty_l);   // R1 free for the pair's dP^T(i+1)
+        stage(v0, 0);
+        stage(v1, 1);
+      }
+    } else if (warp >= 8) {
+      // -------------------------------------------------------------- compute warpgroups (as v2)
+      const int cw = (warp - 8) / 4;
+      const int wq = warp % 4;
+      const int kr = wq * 32 + lane;
+      const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+      const int key_pos = k0 + kr;
+      const f2_t sl2x2 = f2(a.scale_log2, a.scale_log2);
+      const uint32_t p_ready_l = mapa_shared(bar_p_ready, 0), ds_pair_l = mapa_shared(bar_ds_pair, 0);
+      Walk w = walk0;
+      for (int i = 0; i < n; ++i, w.next()) {
+        const int st = i & 1;
+        const int qbase = a.j * a.c + w.qt * BQ;
+        uint32_t pk[32];
+        // ---- phase A: P^T = exp2(S^T sigma log2e - LSE log2e) -> bf16 over R0
+        mbar_wait(bar_st_full(st), (i >> 1) & 1);
+        mbar_wait(bar_s_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          const int c = 64 * cw + 32 * sub;
+          uint32_t sv[32];
+          float p[32];
+          tmem_ld32(tmem + lane_addr + R0 + c, sv);
+          tmem_wait_ld();
+          const uint32_t nl_s = sStats + (st * 2 * BQ + c) * 4;
+          const int qpos0 = qbase + c;
+          const bool masked = (k0 + wq * 32 + 31) > qpos0;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 L = ld_shared_f4(nl_s + c4 * 16);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int c2 = c4 * 4 + h2 * 2;
+              const f2_t x = ffma2(f2u(sv[c2], sv[c2 + 1]), sl2x2, h2 ? f2(L.z, L.w) : f2(L.x, L.y));
+              float p0 = ex2(f2lo(x)), p1 = ex2(f2hi(x));
+              if (masked) {
+                if (key_pos > qpos0 + c2) p0 = 0.f;
+                if (key_pos > qpos0 + c2 + 1) p1 = 0.f;
+              }
+              p[c2] = p0;
+              p[c2 + 1] = p1;
+            }
+          }
+#pragma unroll
+          for (int k2 = 0; k2 < 2; ++k2) {
+            uint32_t pp[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              pp[q] = pack_bf16(p[16 * k2 + 2 * q], p[16 * k2 + 2 * q + 1]);
+              pk[16 * sub + 8 * k2 + q] = pp[q];
+            }
+            tmem_st8(tmem + lane_addr + R0 + c + 16 * k2, pp);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(p_ready_l);
+        // ---- phase B: dS^T = P^T o (dP^T - D) -> bf16 to smem
+        mbar_wait(bar_dp_full, i & 1);
+        tc_fence_after();
+        uint32_t dpv[64];
+        tmem_ld32(tmem + lane_addr + R1 + 64 * cw, *reinterpret_cast<uint32_t(*)[32]>(dpv));
+        tmem_ld32(tmem + lane_addr + R1 + 64 * cw + 32, *reinterpret_cast<uint32_t(*)[32]>(dpv + 32));
+        tmem_wait_ld();
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          const int c = 64 * cw + 32 * sub;
+          const uint32_t d_s = sStats + (st * 2 * BQ + BQ + c) * 4;
+          uint32_t dd[16];
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 Dv = ld_shared_f4(d_s + c4 * 16);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int c2 = c4 * 4 + h2 * 2;
+              const uint32_t pw = pk[16 * sub + c2 / 2];
+              const f2_t p2 = f2(__uint_as_float(pw << 16), __uint_as_float(pw & 0xffff0000u));
+              const f2_t ds2 = fmul2(p2, fsub2(f2u(dpv[32 * sub + c2], dpv[32 * sub + c2 + 1]),
+                                               h2 ? f2(Dv.z, Dv.w) : f2(Dv.x, Dv.y)));
+              dd[c2 / 2] = pack_bf16_f2(ds2);
+            }
+          }
+          const uint32_t drow = sDS + (c / 64) * kBox;
+          const int ch = (c % 64) / 8;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(drow + sw128_off(kr, ch + q), dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]);
+        }
+        tmem_wait_st();
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bar_ds_ready);
+          mbar_arrive_remote(ds_pair_l);
+        }
+      }
+      // ---- epilogue: WG 0 -> dK, WG 1 -> dV (this CTA's keys)
+      mbar_wait(bar_acc, 0);
+      mbar_wait(bar_drain_done, 0);
+      tc_fence_after();
+      const int mat = cw;
+      const float sc = mat == 0 ? a.dk_scale : a.dv_scale;
+      auto stg_box = [&](int cc) { return (mat == 0 ? sb + kQ : sDO) + (uint32_t)cc * kBox; };
+#pragma unroll 1
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_addr + (mat == 0 ? TM_DK : TM_DV) + cc * 32, v);
+        tmem_wait_ld();
+        const uint32_t box = stg_box(cc);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          st_shared_v4(box + sw128_off(kr, q), __float_as_uint(sc * __uint_as_float(v[4 * q])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 1])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 2])),
+                       __float_as_uint(sc * __uint_as_float(v[4 * q + 3])));
+      }
+      fence_async_smem();
+      named_bar_sync(2 + mat, 128);
+      if (wq == 0 && lane == 0) {
+        const int row0 = (mat * a.hkv + g) * a.S + k0;
+        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && row0 + BKV <= 2 * a.hkv * a.S, 514);
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
+        bulk_commit();
+        bulk_wait0();
+      }
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                      // neither CTA leaves while the pair still uses its smem / TMEM
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<512>(tmem);
+}
+
 namespace {
 // ---- work list for one backward call (host side) ------------------------------------------
 // Units (key tile u of kv-head g) cost G * (query tiles that see the tile) 128x128 blocks: the
@@ -1025,11 +1487,14 @@ float list_makespan(std::vector<float> t, const std::vector<float>& pieces) {
   return *std::max_element(t.begin(), t.end());
 }
 
-Schedule compute_schedule(int c, int j, int hkv, int G, int P) {
-  const int nqt = c / bwd::BQ, ntiles = (j + 1) * c / bwd::BKV, N = ntiles * hkv;
+// pair = true: units are pairs of adjacent key tiles run by a cluster of 2 CTAs (P / 2 machines),
+// costed by the query walk of their first tile
+Schedule compute_schedule(int c, int j, int hkv, int G, int P, bool pair = false) {
+  const int nqt = c / bwd::BQ, ntiles = (j + 1) * c / bwd::BKV / (pair ? 2 : 1), N = ntiles * hkv;
+  if (pair) P /= 2;
   const float o = item_overhead();
   auto unit_blocks = [&](int U) {
-    const int rel = (U / hkv) * bwd::BKV - j * c;
+    const int rel = (U / hkv) * bwd::BKV * (pair ? 2 : 1) - j * c;
     return G * (nqt - (rel > 0 ? rel / bwd::BQ : 0));
   };
   auto add_pieces = [&](std::vector<float>& out, int U, int f) {
@@ -1087,16 +1552,16 @@ Schedule compute_schedule(int c, int j, int hkv, int G, int P) {
   return best;
 }
 
-Schedule choose_schedule(int c, int j, int hkv, int G, int P) {
+Schedule choose_schedule(int c, int j, int hkv, int G, int P, bool pair = false) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int, int>, Schedule> cache;
-  const auto key = std::make_tuple(c, j, hkv, G, P);
+  static std::map<std::tuple<int, int, int, int, int, int>, Schedule> cache;
+  const auto key = std::make_tuple(c, j, hkv, G, P, (int)pair);
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
   }
-  const Schedule s = compute_schedule(c, j, hkv, G, P);
+  const Schedule s = compute_schedule(c, j, hkv, G, P, pair);
   std::lock_guard<std::mutex> lk(mu);
   cache.emplace(key, s);
   return s;
@@ -1110,11 +1575,12 @@ extern "C" int32_t seco_debug_bwd_schedule(int32_t c, int32_t j, int32_t hkv, in
 }
 
 cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tdo,
+                             const CUtensorMap& tq64, const CUtensorMap& tdo64,
                              const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tdq,
                              const CUtensorMap& tdkv, const void* o, const void* d_o,
                              const float* lse, float relay, float gscale, float* dkv, void* dq, void* dk_own,
                              void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st, int* launches) {
-  static_assert(bwd::kBytes <= 232448 && bwd2::kBytes <= 232448, "shared memory budget");
+  static_assert(bwd::kBytes <= 232448 && bwd2::kBytes <= 232448 && bwd3::kBytes <= 232448, "shared memory budget");
   // d = 64 runs on zero-padded 128-column tiles (TMA out-of-bounds fill on load; the dK/dV
   // reduce-add boxes past column 64 are dropped by the same bounds check; dQacc rows are 128)
   if ((g.d != bwd::D && g.d != 64) || g.c % bwd::BQ) return cudaErrorInvalidValue;
@@ -1150,11 +1616,17 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   }
 #endif
   const int ntiles = (g.j + 1) * g.c / bwd::BKV;
+  // CTA pairs (v3, cta_group::2 MMAs over two adjacent key tiles) need an even number of key tiles
+  const bool pair = use_v2 && ntiles % 2 == 0 && bwd_uses_pair(g);
+  static std::atomic<unsigned long long> attr_done3{0};
+  if (pair && (e = ensure_smem_attr(seco_bwd3_sm100_kernel, bwd3::kBytes, attr_done3)) != cudaSuccess) return e;
   const Schedule sc = g.det ? Schedule{ntiles * g.hkv, 0, 1, 1, ntiles * g.hkv}   // one owner per dK/dV tile
-                           : choose_schedule(g.c, g.j, g.hkv, a.G, num_sms());
+                           : choose_schedule(g.c, g.j, g.hkv, a.G, num_sms(), pair);
   a.n0 = sc.n0; a.n1 = sc.n1; a.f1 = sc.f1; a.f2 = sc.f2;
-  dim3 grid(sc.grid);
-  if (use_v2)
+  dim3 grid(sc.grid * (pair ? 2 : 1));
+  if (pair)
+    seco_bwd3_sm100_kernel<<<grid, bwd3::kThreads, bwd3::kBytes, st>>>(tq, tdo, tq64, tdo64, tk, tv, tdkv, a);
+  else if (use_v2)
     seco_bwd2_sm100_kernel<<<grid, bwd2::kThreads, bwd2::kBytes, st>>>(tq, tdo, tk, tv, tdkv, a);
   else
     seco_bwd_sm100_kernel<<<grid, bwd::kThreads, bwd::kBytes, st>>>(tq, tdo, tk, tv, tdq, tdkv, a);
@@ -1162,6 +1634,16 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   e = launch_final_bf16(g, ws_dqacc, dq, dkv, dk_own, dv_own, gscale * g.scale, st);
   *launches = 2 + 1;
   return e;
+}
+
+bool bwd_uses_pair(const ChunkGeom& g) {
+  // SECO_BWD_PAIR=1 selects the CTA-pair backward (v3), =0 the single-CTA v2 (A/B switch)
+  static const int mode = [] {
+    const char* e = std::getenv("SECO_BWD_PAIR");
+    return e == nullptr ? -1 : (e[0] == '0' ? 0 : 1);
+  }();
+  const bool on = mode >= 0 ? mode == 1 : SECO_BWD_PAIR_DEFAULT != 0;
+  return on && !g.det && (g.d == 128 || g.d == 64);
 }
 
 unsigned long long check_word_bwd() { return seco_check_read_clear(); }

@@ -45,7 +45,9 @@ bool fwd_uses_pair(const ChunkGeom& g);
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
                              cudaStream_t st, int* launches);
+bool bwd_uses_pair(const ChunkGeom& g);   // CTA-pair backward (v3) selected
 cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tdo,
+                             const CUtensorMap& tq64, const CUtensorMap& tdo64,
                              const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tdq,
                              const CUtensorMap& tdkv, const void* o, const void* d_o,
                              const float* lse, float relay, float gscale, float* dkv, void* dq,

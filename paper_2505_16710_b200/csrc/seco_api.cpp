@@ -284,16 +284,21 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(d_o) || !aligned16(dq))
     return fail(SECO_ERR_ARG, "bf16 tensors must be 16-byte aligned");
   const int S_used = (j + 1) * s->chunk;
-  CUtensorMap tq, tdo, tk, tv, tdq, tdkv;
+  CUtensorMap tq, tdo, tq64, tdo64, tk, tv, tdq, tdkv;
   const int64_t S = (int64_t)s->chunk * s->num_chunks;
+  // 64-row boxes of Q / dO: the CTA-pair backward loads each CTA's query half (seco::bwd_uses_pair)
+  const bool bpair = seco::bwd_uses_pair(g);
   if (!encode_3d(&tq, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 128) ||
       !encode_3d(&tdo, d_o, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 128) ||
+      (bpair && !encode_3d(&tq64, q, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64)) ||
+      (bpair && !encode_3d(&tdo64, d_o, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64)) ||
       !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
       !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
       !encode_f32_rows(&tdq, ws_dqacc, (int64_t)s->hq * s->chunk, 128) ||
       !encode_f32_rows(&tdkv, dkv, 2 * (int64_t)s->hkv * S, 128, s->d))
     return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  e = seco::launch_bwd_sm100(g, tq, tdo, tk, tv, tdq, tdkv, o, d_o, lse, relay_scale, grad_scale, dkv, dq, dk_own, dv_own,
+  if (!bpair) { tq64 = tq; tdo64 = tdo; }
+  e = seco::launch_bwd_sm100(g, tq, tdo, tq64, tdo64, tk, tv, tdq, tdkv, o, d_o, lse, relay_scale, grad_scale, dkv, dq, dk_own, dv_own,
                              ws_dqacc, ws_D, cs, &launches);
   if (e != cudaSuccess) return cuda_fail(e, "bwd_sm100");
   g_launches = launches;

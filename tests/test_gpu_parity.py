@@ -428,3 +428,37 @@ print("pair switch ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, SECO_FWD_PAIR=pair),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "pair switch ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_bf16_backward_pair_subprocess():
+    """The CTA-pair backward (SECO_BWD_PAIR=1: seco_bwd3_sm100_kernel, clusters of two adjacent key
+    tiles, S^T / dP^T / dV / dK as cta_group::2 MMAs with half of every B operand per CTA, dQ^T per
+    CTA; an A/B path) against the oracle on small shapes (d = 64 included), in a child
+    process because the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, torch
+sys.path.insert(0, ".")
+from oracle import chunkwise as OC
+from tests.gpu_util import BF16_TOL, err, host, inputs, upload
+from paper_2505_16710_b200.step import ChunkedAttention
+for (hq, hkv, seq, c, d) in ((8, 2, 512, 256, 128), (8, 2, 1024, 256, 128), (4, 1, 2048, 512, 128),
+                             (8, 2, 1024, 256, 64)):
+    x = inputs(hq, hkv, seq, d, seed=5, peaky=True)
+    q, k, v, do = upload(x, torch.bfloat16)
+    L = ChunkedAttention(hq, hkv, d, seq, c, dtype=torch.bfloat16)
+    L.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    ref = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (seq // c))
+    dk, dv = L.own_grads()
+    for name, gpu in (("dq", host(L.dq)), ("dk", host(dk)), ("dv", host(dv))):
+        e = err(gpu, ref[name])
+        assert e <= BF16_TOL, (hq, hkv, seq, c, d, name, e)
+print("pair bwd ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, SECO_BWD_PAIR="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "pair bwd ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
