@@ -24,7 +24,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 python bench.py --profile-steps 2 > ${P}_ncu_plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:seco_bwd2_sm100 --launch-skip 16 --launch-count 1 \
     -o ${P}_bwd_j15 python bench.py --profile-steps 2 > ${P}_ncu_bwd.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:seco_fwd_sm100 --launch-skip 48 --launch-count 1 \
+ncu --set full --clock-control none --import-source on -k regex:seco_fwd2?_sm100 --launch-skip 48 --launch-count 1 \
     -o ${P}_fwd_j15 python bench.py --profile-steps 2 > ${P}_ncu_fwd.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:lora -s 20 -c 2 -o ${P}_lora \
     python tools/lora_bench.py 2048 4096 4096 8 > ${P}_ncu_lora.log 2>&1
