@@ -157,6 +157,30 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
   const int lane = threadIdx.x % 32;
   if (bid < a.nQ) {
     if (dqacc == nullptr) return;
+    if (dv4 == 32) {
+      // d = 128: one float4 per (row, lane); a thread keeps 4 rows' loads in flight before its
+      // stores (32-bit index math: row = idx >> 5)
+      const int rows = a.hq * a.c, total = rows * 32, stride = a.nQ * (int)blockDim.x;
+      constexpr int U = 4;
+      for (int base = bid * (int)blockDim.x + (int)threadIdx.x; base < total; base += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * stride;
+          if (idx < total) v[u] = reinterpret_cast<const float4*>(dqacc)[(int64_t)(idx >> 5) * ld4 + (idx & 31)];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * stride;
+          if (idx >= total) break;
+          const int row = idx >> 5, h = row / a.c, r = row - h * a.c;
+          float4 w = v[u];
+          w.x *= a.dq_scale; w.y *= a.dq_scale; w.z *= a.dq_scale; w.w *= a.dq_scale;
+          Vec4<T>::store(dq + (int64_t)h * a.qh + (int64_t)r * a.qr + 4 * (idx & 31), w);
+        }
+      }
+      return;
+    }
     // one warp per row (h, r) in a grid-stride loop, 4 rows in flight; lanes stride the row's
     // float4s (no 64-bit index divisions in the loop)
     const int rows = a.hq * a.c;
@@ -179,6 +203,31 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
     }
   } else {
     if (dk_own == nullptr && dv_own == nullptr) return;
+    if (dv4 == 32 && dk_own != nullptr && dv_own != nullptr) {
+      // d = 128, both copies: flat float4 index over (tensor x kv head, row, lane), 4 in flight
+      const int rows = 2 * a.hkv * a.c, total = rows * 32, stride = a.nO * (int)blockDim.x;
+      constexpr int U = 4;
+      for (int base = (bid - a.nQ) * (int)blockDim.x + (int)threadIdx.x; base < total; base += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * stride;
+          if (idx < total) {
+            const int row = idx >> 5, th = row / a.c, r = row - th * a.c;
+            v[u] = reinterpret_cast<const float4*>(dkv + (int64_t)th * a.S * a.d + ((int64_t)a.j * a.c + r) * a.d)[idx & 31];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * stride;
+          if (idx >= total) break;
+          const int row = idx >> 5, th = row / a.c, r = row - th * a.c;
+          T* own = th < a.hkv ? dk_own : dv_own;
+          Vec4<T>::store(own + ((int64_t)(th % a.hkv) * a.c + r) * a.d + 4 * (idx & 31), v[u]);
+        }
+      }
+      return;
+    }
     // rows of slot j: (tensor, kv head, row) -> own copy [hkv][c][d]
     const int rows = 2 * a.hkv * a.c;
     const int gw = (bid - a.nQ) * 8 + threadIdx.x / 32, nw = a.nO * 8;
