@@ -86,7 +86,12 @@ struct Layout {
 
 struct Args {
   int c, j, hq, G, nqt, nhp;  // chunk size, chunk index, q heads, group size, q tiles, head packs
-  int nsplit;                 // split-KV factor (1: final O/LSE written directly)
+  int nsplit;                 // split-KV factor of the units past n_full (1: no split)
+  int n_full;                 // work items [0, n_full) are whole units (final O / LSE written
+                              // directly); the rest are nsplit key-range pieces per unit
+  int n_units;                // work units (query tile x head pack, or x head quad for pairs)
+  int merge;                  // 1: the split units' last pieces merge in-kernel (DP + split
+                              // tail); 0: the combine kernel merges (sub-wave split)
   int d_out;                  // head dim of the O buffer (64: the D = 128 tile is zero-padded)
   int wait_prev;              // PDL launch without SECO_FLAG_PREV_INDEPENDENT: wait for the
                               // predecessor grid before the first global access
@@ -94,11 +99,133 @@ struct Args {
   int64_t qh, qr;             // o strides (elements)
   float* part_o;              // nsplit > 1: [nsplit][hq][c][D] fp32 normalised partial O
   float* part_lse;            // nsplit > 1: [nsplit][hq][c] partial LSE (natural log)
+  int* cnt;                   // nsplit > 1: pieces done per split CTA-unit (zeroed before launch)
   unsigned long long* trace;  // SECO_TRACE builds only: [kTraceCtas][kTraceSlots][kTraceIters]
 };
 #ifdef SECO_TRACE
 constexpr int kTraceCtas = 2, kTraceSlots = 24, kTraceIters = 256;
 #endif
+
+// weak global loads that skip L1: data other CTAs of this grid wrote (after the acquire fence).
+// __ldcg compiles to a strong (LDG.STRONG.GPU) load, which ptxas does not batch.
+__device__ __forceinline__ float4 ld_na_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_na_f32(const float* p) {
+  float v;
+  asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ctaid_x() {   // a fresh read (volatile: not CSE'd with earlier ones)
+  uint32_t x;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(x));
+  return x;
+}
+
+// work item w -> (unit, key-range piece, pieces of that unit): [0, n_full) whole units, then
+// the pieces of the remaining units, piece-major (every unit's first key range, then every
+// unit's second, ...) so the CTAs running at the same time stream the same K/V tiles
+// through L2, as the whole units of a wave do
+struct Work {
+  int unit, split, ns;
+};
+__device__ __forceinline__ Work decode_work(int w, const Args& a) {
+  if (w < a.n_full) return Work{w, 0, 1};
+  const int r = w - a.n_full, rem = a.n_units - a.n_full;
+  return Work{a.n_full + r % rem, r / rem, a.nsplit};
+}
+
+// Split-KV merge (§8 a9), in two steps.  piece_done: every softmax thread (NH warpgroups) of a
+// piece calls it after storing its normalised partial rows (O_s, LSE_s); the piece that
+// completes its CTA-unit last (counter ci) sets the flag.  Release: every thread fences its own
+// stores before the barrier that precedes the counter increment; acquire: the last piece's
+// counting thread fences after observing the count, and every merging thread fences again.
+template <int NH>
+__device__ __forceinline__ void piece_done(const Args& a, int ci, int ns, volatile int* s_flag) {
+  constexpr uint32_t kBarMerge = 7;
+  __threadfence();
+  named_bar_sync(kBarMerge, 128 * NH);
+  if (threadIdx.x % (128 * NH) == 0) {
+    const bool last = atomicAdd(a.cnt + ci, 1) == ns - 1;
+    if (last) __threadfence();
+    *s_flag = last ? 1 : 0;
+  }
+}
+// merge_rows: after the CTA's final barrier, the last piece merges rows of heads h_first ..
+// h_first + NH - 1, query rows row0 .. row0 + 127:
+//   O = sum_s e^{LSE_s - LSE} O_s,  LSE = log sum_s e^{LSE_s},
+// reading all parts back in part order, so the result does not depend on which piece came
+// last (the stage-2 rebuild reproduces stage 1 bit for bit).  The parts, written by other SMs
+// (possibly on the other die), come in by bulk copies into the now idle shared memory (sbuf,
+// >= 2 x 66 KiB + 16 B): 32-row chunks of every part's O rows and LSE, double-buffered; then
+// one warp per row, each lane 4 of the 128 columns.  (Register-staged loads of the same data
+// took ~15 us per merging CTA: too few bytes in flight to cover the cross-die latency.)
+template <int NH>
+__device__ __forceinline__ void merge_rows(const Args& a, int ns, int h_first, int row0, uint32_t sbuf,
+                                           __nv_bfloat16* __restrict__ o, float* __restrict__ lse) {
+  constexpr int kRows = 32, kChunks = NH * 128 / kRows;
+  constexpr uint32_t kPartO = kRows * 128 * 4;               // one part's O rows of a chunk (16 KiB)
+  constexpr uint32_t kBuf = 4 * kPartO + 4 * kRows * 4;       // <= 4 parts' O rows + LSE
+  const uint32_t bar = sbuf + 2 * kBuf;
+  const int64_t plane = (int64_t)a.hq * a.c;
+  auto first_row = [&](int ch) { return (int64_t)(h_first + ch * kRows / 128) * a.c + row0 + ch * kRows % 128; };
+  auto issue = [&](int ch) {                                  // one thread
+    const int64_t w0 = first_row(ch);
+    const uint32_t b = bar + 8 * (ch & 1), dst = sbuf + (ch & 1) * kBuf;
+    mbar_expect_tx(b, ns * (kPartO + kRows * 4));
+    for (int p = 0; p < ns; ++p) {
+      bulk_load(dst + p * kPartO, a.part_o + (p * plane + w0) * 128, kPartO, b);
+      bulk_load(dst + 4 * kPartO + p * kRows * 4, a.part_lse + p * plane + w0, kRows * 4, b);
+    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 8, 1);
+    fence_barrier_init();
+    __threadfence();                                          // acquire, as the counting thread did
+    fence_proxy_async_global();                               // other SMs' generic stores -> bulk reads
+    issue(0);
+    if (kChunks > 1) issue(1);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x % 32, wid = threadIdx.x / 32, nw = blockDim.x / 32;
+#pragma unroll 1
+  for (int ch = 0; ch < kChunks; ++ch) {
+    mbar_wait(bar + 8 * (ch & 1), (ch >> 1) & 1);
+    const uint32_t src = sbuf + (ch & 1) * kBuf;
+    const int64_t w0 = first_row(ch);
+#pragma unroll 1
+    for (int k = wid; k < kRows; k += nw) {
+      float lp[4], mx = -INFINITY, den = 0.f;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        lp[p] = p < ns ? ld_shared_f32(src + 4 * kPartO + (p * kRows + k) * 4) : -INFINITY;
+        mx = fmaxf(mx, lp[p]);
+      }
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        if (p >= ns) break;
+        const float wk = __expf(lp[p] - mx);
+        den += wk;
+        const float4 v = ld_shared_f4(src + p * kPartO + k * 512 + 16 * lane);
+        acc.x += wk * v.x; acc.y += wk * v.y; acc.z += wk * v.z; acc.w += wk * v.w;
+      }
+      const float inv = 1.f / den;
+      const int64_t w = w0 + k;                               // = h * c + row (a chunk stays in one head)
+      if (4 * lane < a.d_out)
+        *reinterpret_cast<uint2*>(o + (w / a.c) * a.qh + (w % a.c) * a.qr + 4 * lane) =
+            make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+      if (lane == 0) lse[w] = mx + __logf(den);
+    }
+    __syncthreads();                                          // buffer ch & 1 consumed
+    if (threadIdx.x == 0 && ch + 2 < kChunks) issue(ch + 2);
+  }
+}
 }  // namespace fwd
 
 template <int NH, int D, int STAGES>
@@ -134,17 +261,20 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
 #else
 #define FTRACE(slot, i) do { } while (0)
 #endif
-  // heavier query tiles first (longest-processing-time order); split-KV part innermost
-  const int unit = (int)blockIdx.x / a.nsplit, split = (int)blockIdx.x % a.nsplit;
+  // heavier query tiles first (longest-processing-time order): whole units, then the pieces of
+  // the split ones (split-KV part innermost)
+  const fwd::Work wk = fwd::decode_work((int)blockIdx.x, a);
+  const int unit = wk.unit, split = wk.split, ns = wk.ns;
   const int qt = a.nqt - 1 - unit / a.nhp;
   const int hp = unit % a.nhp;
   const int h0 = hp * NH, g = h0 / a.G;
   const int q0 = a.j * a.c + qt * fwd::BM;  // absolute position of the tile's first row
   const int T = q0 / fwd::BN + 1;           // K/V tiles 0..T-1; tile T-1 is the causal diagonal
-  const int t0 = T * split / a.nsplit;      // this CTA's K/V tiles: [t0, t0 + nT)
-  const int nT = T * (split + 1) / a.nsplit - t0;
+  const int t0 = T * split / ns;            // this CTA's K/V tiles: [t0, t0 + nT)
+  const int nT = T * (split + 1) / ns - t0;
 
   if (threadIdx.x == 0) {
+    *reinterpret_cast<volatile int*>(smem + L::kTmemSlot + 8) = 0;   // split-KV: "this piece merges"
     for (int b = 0; b < NH; ++b) mbar_init(bar_q(b), 1);
     for (int s = 0; s < STAGES; ++s) { mbar_init(bar_kv_full(s), 1); mbar_init(bar_kv_empty(s), 1); }
     for (int b = 0; b < NH; ++b) {
@@ -419,12 +549,15 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     mbar_wait(bar_o_full(b), (nT - 1) & 1);
     tc_fence_after();
     // epilogue: O = acc / l, LSE = (m + log2 l) ln 2 -- bf16 O directly, or (split-KV) the
-    // normalised fp32 partial for the combine kernel
-    const int h = h0 + b;
+    // normalised fp32 partial for the in-kernel merge.  Indices re-derived from the block index:
+    // keeps them out of the registers of the softmax loop (168-register cap)
+    const fwd::Work we = fwd::decode_work((int)fwd::ctaid_x(), a);
+    const int hf = (we.unit % a.nhp) * NH, row0 = (a.nqt - 1 - we.unit / a.nhp) * fwd::BM;
+    const int h = hf + b, row = row0 + r;
     const float inv_l = 1.f / l;
     const float lse_v = (m + __log2f(l)) * 0.69314718055994531f;
-    if (a.nsplit == 1) {
-      __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)(qt * fwd::BM + r) * a.qr;
+    if (we.ns == 1) {
+      __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)row * a.qr;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         if (cc * 32 >= a.d_out) break;       // warp-uniform
@@ -442,10 +575,10 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           dst[q] = w;
         }
       }
-      SECO_CHECK_COND(h < a.hq && qt * fwd::BM + r < a.c, 520);
-      lse[(int64_t)h * a.c + qt * fwd::BM + r] = lse_v;
+      SECO_CHECK_COND(h < a.hq && row < a.c, 520);
+      lse[(int64_t)h * a.c + row] = lse_v;
     } else {
-      const int64_t prow = ((int64_t)split * a.hq + h) * a.c + qt * fwd::BM + r;
+      const int64_t prow = ((int64_t)we.split * a.hq + h) * a.c + row;
       SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.c, 521);
       float4* dst = reinterpret_cast<float4*>(a.part_o + prow * D);
 #pragma unroll
@@ -459,6 +592,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
                                         __uint_as_float(v[4 * q + 2]) * inv_l, __uint_as_float(v[4 * q + 3]) * inv_l);
       }
       a.part_lse[prow] = lse_v;
+      if (a.merge)
+        fwd::piece_done<NH>(a, we.unit - a.n_full, we.ns, reinterpret_cast<volatile int*>(smem + L::kTmemSlot + 8));
     }
   }
   __syncwarp();
@@ -466,6 +601,11 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<L::kTmemCols>(tmem);
+  if (*reinterpret_cast<volatile int*>(smem + L::kTmemSlot + 8)) {   // the last piece of a split unit
+    const fwd::Work we = fwd::decode_work((int)fwd::ctaid_x(), a);
+    fwd::merge_rows<NH>(a, we.ns, (we.unit % a.nhp) * NH, (a.nqt - 1 - we.unit / a.nhp) * fwd::BM, sbase, o,
+                        lse);
+  }
 #if SECO_FWD_PDL
   // do not complete before the kernel this one may have overlapped: keeps "this grid is done"
   // implying "everything before it in the stream is done" for the plain launches that follow
@@ -530,19 +670,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  // heavier query tiles first; split-KV part innermost; the pair shares (query tile, head quad)
-  const int pair = (int)blockIdx.x / 2;
-  const int unit = pair / a.nsplit, split = pair % a.nsplit;
+  // heavier query tiles first, whole units before pieces (split-KV part innermost); the pair
+  // shares (query tile, head quad)
+  const fwd::Work wk = fwd::decode_work((int)blockIdx.x / 2, a);
+  const int unit = wk.unit, split = wk.split, ns = wk.ns;
   const int nquad = a.hq / 4;
   const int qt = a.nqt - 1 - unit / nquad;
   const int quad = unit % nquad;
   const int h0 = quad * 4 + 2 * (int)rank, g = (quad * 4) / a.G;
   const int q0 = a.j * a.c + qt * BM;
   const int T = q0 / BN + 1;
-  const int t0 = T * split / a.nsplit;
-  const int nT = T * (split + 1) / a.nsplit - t0;
+  const int t0 = T * split / ns;
+  const int nT = T * (split + 1) / ns - t0;
 
   if (threadIdx.x == 0) {
+    *reinterpret_cast<volatile int*>(smem + L::kTmemSlot + 8) = 0;   // split-KV: "this piece merges"
     for (int b = 0; b < NH; ++b) mbar_init(bar_q(b), 1);
     for (int s = 0; s < STAGES; ++s) { mbar_init(bar_kv_full(s), 1); mbar_init(bar_kv_empty(s), 1); }
     for (int b = 0; b < NH; ++b) {
@@ -767,11 +909,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
     }
     mbar_wait(bar_o_full(b), (nT - 1) & 1);
     tc_fence_after();
-    const int h = h0 + b;
+    // epilogue indices re-derived from the block index: keeps them out of the registers of the
+    // softmax loop (this kernel sits at its 168-register cap)
+    const fwd::Work we = fwd::decode_work((int)fwd::ctaid_x() / 2, a);
+    const int row = (a.nqt - 1 - we.unit / (a.hq / 4)) * BM + r;
+    const int h = (we.unit % (a.hq / 4)) * 4 + 2 * (int)cluster_ctarank() + b;
     const float inv_l = 1.f / l;
     const float lse_v = (m + __log2f(l)) * 0.69314718055994531f;
-    if (a.nsplit == 1) {
-      __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)(qt * BM + r) * a.qr;
+    if (we.ns == 1) {
+      __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)row * a.qr;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         if (cc * 32 >= a.d_out) break;
@@ -789,10 +935,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
           dst[q] = w;
         }
       }
-      SECO_CHECK_COND(h < a.hq && qt * BM + r < a.c, 522);
-      lse[(int64_t)h * a.c + qt * BM + r] = lse_v;
+      SECO_CHECK_COND(h < a.hq && row < a.c, 522);
+      lse[(int64_t)h * a.c + row] = lse_v;
     } else {
-      const int64_t prow = ((int64_t)split * a.hq + h) * a.c + qt * BM + r;
+      const int64_t prow = ((int64_t)we.split * a.hq + h) * a.c + row;
       SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.c, 523);
       float4* dst = reinterpret_cast<float4*>(a.part_o + prow * D);
 #pragma unroll
@@ -806,6 +952,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
                                         __uint_as_float(v[4 * q + 2]) * inv_l, __uint_as_float(v[4 * q + 3]) * inv_l);
       }
       a.part_lse[prow] = lse_v;
+      if (a.merge)
+        fwd::piece_done<NH>(a, 2 * (we.unit - a.n_full) + (int)cluster_ctarank(), we.ns,
+                            reinterpret_cast<volatile int*>(smem + L::kTmemSlot + 8));
     }
   }
   __syncwarp();
@@ -814,6 +963,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
   cluster_sync();                                    // neither CTA leaves while the pair still uses its smem / TMEM
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair<512>(tmem);
+  if (*reinterpret_cast<volatile int*>(smem + L::kTmemSlot + 8)) {   // the last piece of a split CTA-unit
+    const fwd::Work we = fwd::decode_work((int)fwd::ctaid_x() / 2, a);
+    fwd::merge_rows<NH>(a, we.ns, (we.unit % (a.hq / 4)) * 4 + 2 * (int)cluster_ctarank(),
+                        (a.nqt - 1 - we.unit / (a.hq / 4)) * BM, sbase, o, lse);
+  }
 #if SECO_FWD_PDL
   if (threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
@@ -844,26 +998,51 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.qh = g.qh; a.qr = g.qr; a.d_out = g.d;
   a.wait_prev = g.prev_indep ? 0 : 1;
-  // split-KV (§8 row a9) when the chunk has too few equal-cost units (q tiles x head packs)
-  // to fill the SMs -- e.g. head-sharded ranks.  Cost model in K/V-tile units per wave:
-  // ~8 tiles of prologue/epilogue per work item, 15% of a unit for the fp32 partial
-  // write + combine; measured on B200: a 2-wave grid (cfg3, 256 units) is NOT worth
-  // splitting, a sub-wave grid is.
-  const int units = a.nqt * a.nhp;
-  const int t_min = g.j * g.c / fwd::BN + 1;
+  // split-KV (§8 row a9).  A sub-wave grid (fewer units than work slots: head-sharded ranks,
+  // short chunks) cuts every unit into nsplit key ranges and merges the parts with the combine
+  // kernel.  A multi-wave grid runs DP + split tail: the first n_full units (as many whole waves
+  // as the grid fills) run whole, the remaining ones are cut into nsplit key ranges whose
+  // pieces fill the last waves, and the piece that finishes a unit last merges its parts
+  // in-kernel (there the merges overlap other pieces' work; in a sub-wave grid every merge
+  // would sit on the critical path, where the combine kernel spreads it over all SMs).  Cost
+  // in K/V-tile times per work slot (an SM, or a cluster for the pair kernel): kOver tiles of
+  // prologue / epilogue per CTA; the combine ~0.15 of a unit; kMerge per round of pieces for
+  // the partial rows and the in-kernel merge (measured).  SECO_FWD_NSPLIT=s forces
+  // s; SECO_FWD_SLOTS=n pretends n work slots (tests reach the DP + tail form on small shapes).
+  constexpr double kOver = 8.0, kMerge = 7.0;
+  static const int forced = [] {
+    const char* e = std::getenv("SECO_FWD_NSPLIT");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
+  static const int slots_env = [] {
+    const char* e = std::getenv("SECO_FWD_SLOTS");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
+  const int units = a.nqt * a.nhp / (PAIR ? 2 : 1);   // work units (pairs: 4-head quads)
+  const int sm_slots = slots_env > 0 ? slots_env : fwd::kSMs;
+  const int slots = PAIR ? (sm_slots + 1) / 2 : sm_slots;
+  const int t_min = g.j * g.c / fwd::BN + 1;          // K/V tiles of the lightest unit
+  const int waves_full = units / slots;
+  const int n_full = waves_full * slots, rem = units - n_full;
+  // workspace: partial O [nsplit][hq][c][128] + partial LSE [nsplit][hq][c] + the counters
+  auto cnt_off = [&](int sp) { return (size_t)sp * g.hq * g.c * (D + 1); };
   int best = 1;
-  double best_cost = 1e30;
-  for (int sp = 1; sp <= 4; ++sp) {
-    if (sp > 1 && (t_min < 8 * sp || g.j == 0 || ws == nullptr ||
-                   (size_t)sp * g.hq * g.c * (D + 1) > ws_floats))
-      break;
-    const double waves = (double)((units * sp + fwd::kSMs - 1) / fwd::kSMs);
-    const double cost = waves * ((double)t_min / sp + 8.0) + (sp > 1 ? 0.15 * t_min : 0.0);
-    if (cost < best_cost) { best_cost = cost; best = sp; }
+  double best_cost = (double)((units + slots - 1) / slots) * (t_min + kOver);
+  for (int sp = 2; sp <= 4 && rem > 0; ++sp) {
+    if (t_min < 8 * sp || g.j == 0 || ws == nullptr || cnt_off(sp) + (size_t)2 * units > ws_floats) break;
+    const int rounds = (rem * sp + slots - 1) / slots;
+    const double cost = waves_full * (t_min + kOver) + rounds * ((double)t_min / sp + kOver) +
+                        (waves_full == 0 ? 0.15 * t_min : kMerge * rounds);
+    if (forced ? sp == forced : cost < best_cost) { best_cost = cost; best = sp; }
   }
+  if (forced == 1) best = 1;
   a.nsplit = best;
+  a.n_full = best > 1 ? n_full : units;
+  a.n_units = units;
+  a.merge = best > 1 && n_full > 0 ? 1 : 0;
   a.part_o = ws;
   a.part_lse = ws ? ws + (size_t)best * g.hq * g.c * D : nullptr;
+  a.cnt = ws ? reinterpret_cast<int*>(ws + cnt_off(best)) : nullptr;
   a.trace = nullptr;
 #ifdef SECO_TRACE
   {
@@ -875,8 +1054,13 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
     seco_fwd_trace_buffer = tbuf;
   }
 #endif
-  dim3 grid(units * a.nsplit);
+  const int items = a.n_full + (units - a.n_full) * a.nsplit;
+  dim3 grid(items * (PAIR ? 2 : 1));
   cudaError_t e;
+  if (a.merge) {   // one counter per split CTA-unit (pairs: per CTA of the pair)
+    e = cudaMemsetAsync(a.cnt, 0, sizeof(int) * 2 * (size_t)units, st);
+    if (e != cudaSuccess) return e;
+  }
   if (SECO_FWD_PDL && a.nsplit == 1) {
     // the split path writes fp32 partials into the workspace, which a preceding backward's
     // final kernel may still be reading: only the unsplit forward may overlap its predecessor
@@ -897,7 +1081,7 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   }
   e = cudaGetLastError();
   *launches = 1;
-  if (e == cudaSuccess && a.nsplit > 1) {
+  if (e == cudaSuccess && a.nsplit > 1 && !a.merge) {
     e = launch_fwd_combine(g, a.nsplit, a.part_o, a.part_lse, o, lse, st);
     *launches = 2;
   }

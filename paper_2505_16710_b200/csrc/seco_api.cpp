@@ -182,9 +182,10 @@ size_t ws_floats(const seco_shape* s) {
   // backward: dQ accumulator [hq][c][d] + D [hq][c] + (-LSE log2 e) [hq][c]
   //           + (deterministic mode) dQ order counters [hq][ceil(c/128)] int32 + a work ticket
   // forward (split-KV, up to 4 parts): partial O [4][hq][c][d] + partial LSE [4][hq][c]
+  //           + piece counters, two per 128-row query tile and head
   const size_t bwd = (size_t)s->hq * s->chunk * dq_ld(s) + 2 * (size_t)s->hq * s->chunk +
                      (size_t)s->hq * ((s->chunk + 127) / 128) + 1;
-  const size_t fwd = 4 * (size_t)s->hq * s->chunk * (dq_ld(s) + 1);
+  const size_t fwd = 4 * (size_t)s->hq * s->chunk * (dq_ld(s) + 1) + 2 * (size_t)s->hq * ((s->chunk + 127) / 128);
   return bwd > fwd ? bwd : fwd;
 }
 

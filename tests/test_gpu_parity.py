@@ -172,7 +172,7 @@ def test_bf16_forward_split_kv(j, d):
     layer.forward_chunk(q, k, v, j)
     launches = __import__("paper_2505_16710_b200").ops.last_launch_count()
     torch.cuda.synchronize()
-    assert launches == 2       # split-KV kernel + combine
+    assert launches == 2       # split-KV kernel + combine (a sub-wave grid)
     o_ref, lse_ref = OA.chunk_fwd(x.q[:, j * c:(j + 1) * c], x.k, x.v, j * c)
     assert err(host(layer.o[:, j * c:(j + 1) * c]), o_ref) <= BF16_TOL
     assert err(host(layer.lse[j]), lse_ref) <= 1e-4
@@ -428,6 +428,54 @@ print("pair switch ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, SECO_FWD_PAIR=pair),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "pair switch ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("pair,nsplit", [("0", ""), ("1", ""), ("0", "2"), ("1", "4")])
+def test_bf16_forward_dp_split_tail_subprocess(pair, nsplit):
+    """The DP + split-tail forward (multi-wave grids): whole units first, then the
+    remaining units cut into key-range pieces whose last piece merges in-kernel (counter per
+    CTA-unit, bulk-copied parts).  SECO_FWD_SLOTS=5 pretends 5 work slots so the small parity
+    shapes here are multi-wave grids; SECO_FWD_NSPLIT forces the split factor.  O, LSE and the
+    whole step against the oracle; the stage-2 rebuild reproduces stage 1 bit for bit; one
+    library launch per split forward (no combine kernel).  Read once per process: child."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import chunkwise as OC
+from tests.gpu_util import BF16_TOL, err, host, inputs, upload
+from paper_2505_16710_b200 import ops
+from paper_2505_16710_b200.step import ChunkedAttention
+for (hq, hkv, seq, c, d) in ((8, 2, 4096, 1024, 128), (4, 1, 8192, 2048, 128), (8, 2, 4096, 1024, 64)):
+    x = inputs(hq, hkv, seq, d, seed=11, peaky=True)
+    q, k, v, do = upload(x, torch.bfloat16)
+    L = ChunkedAttention(hq, hkv, d, seq, c, dtype=torch.bfloat16)
+    for j in range(seq // c):
+        L.forward_chunk(q, k, v, j)
+        n = ops.last_launch_count()
+        assert n == 1, (hq, hkv, seq, c, d, j, n)
+    torch.cuda.synchronize()
+    o1, lse1 = L.o.clone(), L.lse.clone()
+    L.seco_step(q, k, v, do)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, L.o) and torch.equal(lse1, L.lse), (hq, hkv, seq, c, d, "rebuild not bitwise")
+    ref = OC.seco_step(x.q, x.k, x.v, x.do, [c] * (seq // c))
+    dk, dv = L.own_grads()
+    for name, gpu in (("o", host(L.o)), ("dq", host(L.dq)), ("dk", host(dk)), ("dv", host(dv))):
+        e = err(gpu, ref[name])
+        assert e <= BF16_TOL, (hq, hkv, seq, c, d, name, e)
+    lse = L.lse_full().cpu().numpy()
+    assert np.abs(lse - ref["lse"]).max() <= 1e-3, (hq, hkv, seq, c, d, "lse")
+print("dp split tail ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SECO_FWD_PAIR=pair, SECO_FWD_SLOTS="5")
+    if nsplit:
+        env["SECO_FWD_NSPLIT"] = nsplit
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "dp split tail ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_bf16_backward_pair_subprocess():
