@@ -1,6 +1,6 @@
 """A/B step timing of library variants (SECO_LIB_VARIANT .so files in the package dir),
 alternated in separate processes so the power-capped clock state is shared fairly.
-usage: python tools/ab_step.py cfg3 libseco_base.so libseco.so [rounds] [ENV=VAL ...per variant via 'lib.so:ENV=VAL']"""
+usage: python tools/ab_step.py cfg3 libseco_base.so,libseco.so [rounds] [ENV=VAL ...per variant via 'lib.so:ENV=VAL']"""
 import os
 import subprocess
 import sys
