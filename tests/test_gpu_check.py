@@ -77,11 +77,15 @@ print("check build clean")
 '''
 
 
-@pytest.mark.parametrize("v2", ["1", "0"])
-def test_check_build_reports_nothing_on_parity_workloads(v2):
+@pytest.mark.parametrize("extra", [{"SECO_BWD_V2": "1"}, {"SECO_BWD_V2": "0"},
+                                   # the DP + split-tail forward (5 pretended work slots) and its
+                                   # in-kernel merge, CTA-pair and single-CTA forward
+                                   {"SECO_FWD_SLOTS": "5", "SECO_FWD_PAIR": "1"},
+                                   {"SECO_FWD_SLOTS": "5", "SECO_FWD_PAIR": "0"}])
+def test_check_build_reports_nothing_on_parity_workloads(extra):
     lib = os.path.join(ROOT, "paper_2505_16710_b200", "libseco_check.so")
     assert os.path.exists(lib), "build it with python -m paper_2505_16710_b200.build --check (__graft_entry__.build)"
-    env = dict(os.environ, SECO_LIB_VARIANT="libseco_check.so", SECO_BWD_V2=v2)
+    env = dict(os.environ, SECO_LIB_VARIANT="libseco_check.so", **extra)
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and "check build clean" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
