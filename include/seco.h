@@ -108,9 +108,13 @@ size_t seco_workspace_size(const seco_shape* shape);
  * must already hold chunk j's keys/values.  `ws` is optional: when it is given
  * (ws_bytes >= seco_workspace_size()), long chunks may split each query tile's
  * key range over several CTAs (split-KV) and merge the partial results with the
- * exact LSE-weighted combine; with ws == NULL no split is used.  Deterministic
- * for a given (shape, j, ws != NULL): the stage-2 rebuild reproduces stage 1
- * bit for bit. */
+ * exact LSE-weighted combine -- by a second kernel when the grid is smaller
+ * than one wave, in-kernel by the last piece of each query tile otherwise (the
+ * call then also enqueues a cudaMemsetAsync of its piece counters in ws); with
+ * ws == NULL no split is used.  ws is scratch: its contents on entry do not
+ * matter and are clobbered; two calls that share a ws must be stream-ordered.
+ * Deterministic for a given (shape, j, ws != NULL): the stage-2 rebuild
+ * reproduces stage 1 bit for bit (parts are merged in part order). */
 seco_status seco_chunk_forward(const seco_shape* shape, int32_t j,
                                const void* q, const void* k_cache, const void* v_cache,
                                void* o, float* lse,
