@@ -29,6 +29,7 @@ SECO_DEV float warp_sum(float v) {
 
 struct PrepArgs {
   int hq, hkv, c, d, j, S;
+  int cp;          // rows per head of D / nlse / dQacc (c, or c rounded up to 128 on the bf16 path)
   int64_t qh, qr;
   float relay;
   int nD, nR, nZ;  // block counts of the three tasks
@@ -81,8 +82,9 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
         for (int off = lpr / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         const int w = w0 + u * rpw + sub;
         if (lane % lpr == 0 && w < nrows) {
-          D[w] = acc;
-          if (nlse) nlse[w] = -1.4426950408889634f * lse[w];
+          const int h = w / a.c, r = w % a.c;
+          D[(int64_t)h * a.cp + r] = acc;
+          if (nlse) nlse[(int64_t)h * a.cp + r] = -1.4426950408889634f * lse[w];
         }
       }
     }
@@ -96,8 +98,8 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
     for (int x = lane; x < a.d; x += 32) acc += ldf(orow + x) * ldf(drow + x);
     acc = warp_sum(acc);
     if (lane == 0) {
-      D[(int64_t)h * a.c + r] = acc;
-      if (nlse) nlse[(int64_t)h * a.c + r] = -1.4426950408889634f * lse[(int64_t)h * a.c + r];
+      D[(int64_t)h * a.cp + r] = acc;
+      if (nlse) nlse[(int64_t)h * a.cp + r] = -1.4426950408889634f * lse[(int64_t)h * a.c + r];
     }
   } else if (bid < a.nD + a.nR) {
     if (a.relay == 1.f) return;
@@ -113,10 +115,19 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
       *p = v;
     }
   } else {
+    if (bid == a.nD + a.nR) {
+      if (a.order)
+        for (int i = threadIdx.x; i < a.n_order; i += blockDim.x) a.order[i] = 0;
+      // padded rows of a ragged last query tile: P = exp2(S sigma log2 e - inf) = 0, dS = 0
+      const int pad = a.cp - a.c;
+      for (int i = threadIdx.x; i < a.hq * pad; i += blockDim.x) {
+        const int64_t w = (int64_t)(i / pad) * a.cp + a.c + i % pad;
+        D[w] = 0.f;
+        if (nlse) nlse[w] = -INFINITY;
+      }
+    }
     if (dqacc == nullptr) return;
-    if (a.order && bid == a.nD + a.nR)
-      for (int i = threadIdx.x; i < a.n_order; i += blockDim.x) a.order[i] = 0;
-    const int64_t total = (int64_t)a.hq * a.c * a.ldq / 4;
+    const int64_t total = (int64_t)a.hq * a.cp * a.ldq / 4;
     float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t i = (int64_t)(bid - a.nD - a.nR) * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)a.nZ * blockDim.x)
@@ -126,6 +137,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
 
 struct FinalArgs {
   int hq, hkv, c, d, j, S;
+  int cp;          // rows per head of dQacc
   int ldq;         // dQacc row stride (floats)
   int64_t qh, qr;
   float dq_scale;  // s * sigma
@@ -167,7 +179,10 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int idx = base + u * stride;
-          if (idx < total) v[u] = reinterpret_cast<const float4*>(dqacc)[(int64_t)(idx >> 5) * ld4 + (idx & 31)];
+          if (idx < total) {
+            const int row = idx >> 5, h = row / a.c, r = row - h * a.c;
+            v[u] = reinterpret_cast<const float4*>(dqacc)[((int64_t)h * a.cp + r) * ld4 + (idx & 31)];
+          }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
         const int row = row0 + u;
         if (row >= rows) break;
         const int h = row / a.c, r = row - h * a.c;
-        const float4* src = reinterpret_cast<const float4*>(dqacc) + (int64_t)row * ld4;
+        const float4* src = reinterpret_cast<const float4*>(dqacc) + ((int64_t)h * a.cp + r) * ld4;
         T* dst = dq + (int64_t)h * a.qh + (int64_t)r * a.qr;
         for (int x4 = lane; x4 < dv4; x4 += 32) {
           float4 v = src[x4];
@@ -247,6 +262,7 @@ static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, flo
                                const float* lse, float* nlse, float relay, cudaStream_t st, int* order = nullptr) {
   PrepArgs a;
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
+  a.cp = g.cp > 0 ? g.cp : g.c;
   a.qh = g.qh; a.qr = g.qr; a.relay = relay;
   a.vec = (sizeof(T) == 2 && (g.d == 64 || g.d == 128)) ? 1 : 0;
   a.nD = a.vec ? 296 : (g.hq * g.c + 7) / 8;
@@ -265,6 +281,7 @@ static cudaError_t launch_final(const ChunkGeom& g, const float* dqacc, T* dq, c
   FinalArgs a;
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
   a.qh = g.qh; a.qr = g.qr; a.dq_scale = dq_scale; a.ldq = g.ldq ? g.ldq : g.d;
+  a.cp = g.cp > 0 ? g.cp : g.c;
   a.nQ = dqacc ? 296 : 0;
   a.nO = (dk_own || dv_own) ? 148 : 0;
   if (a.nQ + a.nO == 0) return cudaSuccess;
@@ -371,7 +388,7 @@ cudaError_t launch_chunk_skip(const ChunkGeom& g, bool bf16, float* dkv, void* d
 // O = sum_s exp(LSE_s - LSE) O_s,  LSE = log sum_s exp(LSE_s)   (exact merge of softmax partials
 // over disjoint key ranges).  One warp per (head, row); each lane owns 4 of the d = 128 columns.
 struct CombArgs {
-  int hq, c, nsplit, d;
+  int hq, c, cp, nsplit, d;   // cp: rows per head of the partials (c rounded up to 128)
   int64_t qh, qr;
 };
 __global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restrict__ part_o,
@@ -381,15 +398,15 @@ __global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restric
   const int w = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (w >= a.hq * a.c) return;
   const int h = w / a.c, r = w % a.c;
-  const int64_t plane = (int64_t)a.hq * a.c;
+  const int64_t plane = (int64_t)a.hq * a.cp, pw = (int64_t)h * a.cp + r;   // partial row
   float mx = -INFINITY;
-  for (int s = 0; s < a.nsplit; ++s) mx = fmaxf(mx, part_lse[s * plane + w]);
+  for (int s = 0; s < a.nsplit; ++s) mx = fmaxf(mx, part_lse[s * plane + pw]);
   float den = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = 0; s < a.nsplit; ++s) {
-    const float wt = __expf(part_lse[s * plane + w] - mx);
+    const float wt = __expf(part_lse[s * plane + pw] - mx);
     den += wt;
-    const float4 v = reinterpret_cast<const float4*>(part_o + (s * plane + w) * 128)[lane];
+    const float4 v = reinterpret_cast<const float4*>(part_o + (s * plane + pw) * 128)[lane];
     acc.x += wt * v.x; acc.y += wt * v.y; acc.z += wt * v.z; acc.w += wt * v.w;
   }
   const float inv = 1.f / den;
@@ -404,7 +421,7 @@ __global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restric
 cudaError_t launch_fwd_combine(const ChunkGeom& g, int nsplit, const float* part_o, const float* part_lse, void* o,
                                float* lse, cudaStream_t st) {
   CombArgs a;
-  a.hq = g.hq; a.c = g.c; a.nsplit = nsplit; a.qh = g.qh; a.qr = g.qr; a.d = g.d;
+  a.hq = g.hq; a.c = g.c; a.cp = g.cp; a.nsplit = nsplit; a.qh = g.qh; a.qr = g.qr; a.d = g.d;
   fwd_combine_kernel<<<(g.hq * g.c + 7) / 8, 256, 0, st>>>(part_o, part_lse, reinterpret_cast<__nv_bfloat16*>(o),
                                                             lse, a);
   return cudaGetLastError();

@@ -98,6 +98,7 @@ constexpr int R0 = 0, R1 = 128, TM_DK = 256, TM_DV = 384;
 
 struct Args {
   int c, j, G, hkv, S;
+  int cp;             // rows per head of nlse / Dv / dqacc: c rounded up to BQ (ragged last tile)
   // work list (launch_bwd_sm100 / choose_schedule): blocks [0, n0) take whole units, the next
   // n1 units are split into f1 query-range pieces each, the remaining units into f2 pieces.
   // Unit U = (key tile U / hkv, kv head U % hkv); ascending key tiles = descending work.
@@ -105,10 +106,10 @@ struct Args {
   float scale_log2;   // sigma * log2 e
   float dk_scale;     // s * sigma
   float dv_scale;     // s
-  const float* nlse;  // [hq][c]  -LSE * log2(e)   (from bwd_prep)
-  const float* Dv;    // [hq][c]  rowsum(dO o O)  (from bwd_prep)
-  float* dqacc;       // [hq][c][D] fp32 dQ accumulator (zeroed by bwd_prep)
-  int* dq_order;      // deterministic mode: [hq][c/BQ] count of key tiles that have added their
+  const float* nlse;  // [hq][cp]  -LSE * log2(e)   (from bwd_prep; -inf on padded rows)
+  const float* Dv;    // [hq][cp]  rowsum(dO o O)  (from bwd_prep; 0 on padded rows)
+  float* dqacc;       // [hq][cp][D] fp32 dQ accumulator (zeroed by bwd_prep)
+  int* dq_order;      // deterministic mode: [hq][ceil(c/BQ)] count of key tiles that have added their
                       // dQ share of query tile (h, qt) (zeroed by bwd_prep); null otherwise
   int* ticket;        // deterministic mode: work-unit ticket counter (zeroed by bwd_prep); null otherwise
   int* err;           // set to 1 if the dynamic smem window is not 1024-B aligned
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
   const int g = U % a.hkv;
   const int u = U / a.hkv;
   const int k0 = u * BKV;                                  // first key (absolute position)
-  const int nqt = a.c / BQ;
+  const int nqt = (a.c + BQ - 1) / BQ;
   const int rel = k0 - a.j * a.c;                          // key offset relative to chunk j's first row
   const int qt_min = rel > 0 ? rel / BQ : 0;               // first query tile that sees key k0
   const int n_all = a.G * (nqt - qt_min);
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       // -------------------------------------------------------------- TMA producer
       if (lane == 0) {
         mbar_expect_tx(bar_kv, 2 * kTile);
-        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && g < a.hkv, 410);   // key tile inside slots 0..j
+        SECO_CHECK_COND(k0 < (a.j + 1) * a.c && g < a.hkv, 410);   // key tile inside slots 0..j
         for (int x = 0; x < D / 64; ++x) {
           tma_load_3d(sK + x * kBox, &tm_k, bar_kv, x * 64, k0, g);
           tma_load_3d(sV + x * kBox, &tm_v, bar_kv, x * 64, k0, g);
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           const int st = i & 1;
           const uint32_t ph = (i >> 1) & 1;
           const int h = g * a.G + w.hh, qt = w.qt;
-          SECO_CHECK_COND(qt * BQ + BQ <= a.c && w.hh < a.G, 411);       // query tile inside chunk j
+          SECO_CHECK_COND(qt * BQ < a.c && w.hh < a.G, 411);       // query tile inside chunk j
           // dO first: dP^T(i) is issued before S^T(i), and its buffer frees earlier (dV(i-2))
           mbar_wait(bar_do_empty(st), ph ^ 1);
           mbar_expect_tx(bar_do_full(st), kTile);
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
           mbar_expect_tx(bar_q_full(st), kTile + 2 * BQ * 4);
           for (int x = 0; x < D / 64; ++x)
             tma_load_3d(qbuf(st) + x * kBox, &tm_q, bar_q_full(st), x * 64, qt * BQ, h);
-          const int64_t ro = (int64_t)h * a.c + qt * BQ;
+          const int64_t ro = (int64_t)h * a.cp + qt * BQ;
           bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_q_full(st));
           bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_q_full(st));
           TRACE(0, i);
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
       named_bar_sync(2 + mat, 256);
       if ((wg & 1) == 0 && wq == 0 && lane == 0) {
         const int row0 = (mat * a.hkv + g) * a.S + k0;
-        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && row0 + BKV <= 2 * a.hkv * a.S, 510);   // dKV rows
+        SECO_CHECK_COND(k0 < (a.j + 1) * a.c && row0 < 2 * a.hkv * a.S, 510);   // dKV rows
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
         bulk_commit();
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
         for (int i = 0; i < n; ++i, w.next()) {
           const int st = i & 1;
           const int h = g * a.G + w.hh, qt = w.qt;
-          float* dst = a.dqacc + ((int64_t)h * a.c + qt * BQ) * D;   // 128 contiguous dQacc rows
+          float* dst = a.dqacc + ((int64_t)h * a.cp + qt * BQ) * D;  // 128 contiguous dQacc rows
           // rows 64-127 (in dO(i)'s buffer) first: dP(i+2) needs that buffer before S(i+2) needs Q's
           // (the TMA unit serves requests in order and loads queue behind these; issuing the
           // tile in 4-16 KiB pieces with <= 2 in flight measured 2-20 % slower)
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1)
             fence_acq_rel_gpu();
             fence_proxy_async_global();      // ... before this thread's TMA reduce-adds
           }
-          SECO_CHECK_COND(dst >= a.dqacc && dst + 128 * D <= a.dqacc + (int64_t)a.G * a.hkv * a.c * D, 511);
+          SECO_CHECK_COND(dst >= a.dqacc && dst + 128 * D <= a.dqacc + (int64_t)a.G * a.hkv * a.cp * D, 511);
           bulk_reduce_add_f32(dst + 64 * D, dobuf(st), kTile);
           bulk_commit();
           if (!ctr) mbar_wait(bar_stg_half(0), i & 1);
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
   const int g = U % a.hkv;
   const int u = U / a.hkv;
   const int k0 = u * BKV;
-  const int nqt = a.c / BQ;
+  const int nqt = (a.c + BQ - 1) / BQ;
   const int rel = k0 - a.j * a.c;
   const int qt_min = rel > 0 ? rel / BQ : 0;
   const int n_all = a.G * (nqt - qt_min);
@@ -667,7 +668,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
       // -------------------------------------------------------------- TMA producer
       if (lane == 0) {
         mbar_expect_tx(bar_kv, 2 * kTile);
-        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && g < a.hkv, 410);   // key tile inside slots 0..j
+        SECO_CHECK_COND(k0 < (a.j + 1) * a.c && g < a.hkv, 410);   // key tile inside slots 0..j
         for (int x = 0; x < D / 64; ++x) {
           tma_load_3d(sK + x * kBox, &tm_k, bar_kv, x * 64, k0, g);
           tma_load_3d(sV + x * kBox, &tm_v, bar_kv, x * 64, k0, g);
@@ -677,12 +678,12 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
           const int st = i & 1;
           const uint32_t ph = (i >> 1) & 1;
           const int h = g * a.G + w.hh, qt = w.qt;
-          SECO_CHECK_COND(qt * BQ + BQ <= a.c && w.hh < a.G, 412);       // query tile inside chunk j
+          SECO_CHECK_COND(qt * BQ < a.c && w.hh < a.G, 412);       // query tile inside chunk j
           mbar_wait(bar_q_empty(st), ph ^ 1);
           mbar_expect_tx(bar_q_full(st), kTile + 2 * BQ * 4);
           for (int x = 0; x < D / 64; ++x)
             tma_load_3d(qbuf(st) + x * kBox, &tm_q, bar_q_full(st), x * 64, qt * BQ, h);
-          const int64_t ro = (int64_t)h * a.c + qt * BQ;
+          const int64_t ro = (int64_t)h * a.cp + qt * BQ;
           bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_q_full(st));
           bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_q_full(st));
           V2TRACE(0, i);
@@ -791,11 +792,11 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
         int m = 0;                                        // staged chunk sequence number
         for (int i = 0; i < n; ++i, w.next()) {
           const int h = g * a.G + w.hh, qt = w.qt;
-          float* dst = a.dqacc + ((int64_t)h * a.c + qt * BQ) * D;
+          float* dst = a.dqacc + ((int64_t)h * a.cp + qt * BQ) * D;
           for (int c = 0; c < 4; ++c, ++m) {
             const int s = c & 1;
             mbar_wait(bar_stg_full(s), (m >> 1) & 1);
-            SECO_CHECK_COND(dst >= a.dqacc && dst + 32 * (c + 1) * D <= a.dqacc + (int64_t)a.G * a.hkv * a.c * D, 512);
+            SECO_CHECK_COND(dst >= a.dqacc && dst + 32 * (c + 1) * D <= a.dqacc + (int64_t)a.G * a.hkv * a.cp * D, 512);
             bulk_reduce_add_f32(dst + 32 * c * D, sSTG + s * kSlot, kSlot);
             bulk_commit();
             if (c == 0) V2TRACE(16, i);
@@ -974,7 +975,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1)
       named_bar_sync(2 + mat, 128);
       if (wq == 0 && lane == 0) {
         const int row0 = (mat * a.hkv + g) * a.S + k0;
-        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && row0 + BKV <= 2 * a.hkv * a.S, 510);   // dKV rows
+        SECO_CHECK_COND(k0 < (a.j + 1) * a.c && row0 < 2 * a.hkv * a.S, 510);   // dKV rows
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
         bulk_commit();
@@ -1073,7 +1074,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(bwd3::kThreads, 1)
   const int g = U % a.hkv;
   const int u = 2 * (U / a.hkv) + rank;
   const int k0 = u * BKV;
-  const int nqt = a.c / BQ;
+  const int nqt = (a.c + BQ - 1) / BQ;
   const int rel = 2 * (U / a.hkv) * BKV - a.j * a.c;
   const int qt_min = rel > 0 ? rel / BQ : 0;
   const int n_all = a.G * (nqt - qt_min);
@@ -1124,7 +1125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(bwd3::kThreads, 1)
       // -------------------------------------------------------------- TMA producer (both CTAs)
       if (lane == 0) {
         mbar_expect_tx(bar_kv, 2 * kTile);
-        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && g < a.hkv, 413);
+        SECO_CHECK_COND(k0 < (a.j + 1) * a.c && g < a.hkv, 413);
         for (int x = 0; x < D / 64; ++x) {
           tma_load_3d(sK + x * kBox, &tm_k, bar_kv, x * 64, k0, g);
           tma_load_3d(sV + x * kBox, &tm_v, bar_kv, x * 64, k0, g);
@@ -1134,14 +1135,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(bwd3::kThreads, 1)
           const int st = i & 1;
           const uint32_t ph = (i >> 1) & 1;
           const int h = g * a.G + w.hh, qt = w.qt;
-          SECO_CHECK_COND(qt * BQ + BQ <= a.c && w.hh < a.G, 414);
+          SECO_CHECK_COND(qt * BQ < a.c && w.hh < a.G, 414);
           mbar_wait(bar_q_empty(st), ph ^ 1);
           if (leader) mbar_expect_tx(bar_q_full(st), 2 * kQStage);
           const uint32_t bq = mapa_shared(bar_q_full(st), 0);
           for (int x = 0; x < D / 64; ++x)      // Qr: this CTA's 64 query rows, all d
             tma_load_3d_pair(qbuf(st) + x * kHalf, &tm_q64, bq, x * 64, qt * BQ + 64 * rank, h, kHalf);
           tma_load_3d_pair(qbuf(st) + 2 * kHalf, &tm_q, bq, 64 * rank, qt * BQ, h, kBox);   // Qc
-          const int64_t ro = (int64_t)h * a.c + qt * BQ;
+          const int64_t ro = (int64_t)h * a.cp + qt * BQ;
           mbar_expect_tx(bar_st_full(st), 2 * BQ * 4);
           bulk_load(sStats + st * 2 * BQ * 4, a.nlse + ro, BQ * 4, bar_st_full(st));
           bulk_load(sStats + st * 2 * BQ * 4 + BQ * 4, a.Dv + ro, BQ * 4, bar_st_full(st));
@@ -1255,11 +1256,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(bwd3::kThreads, 1)
         int m = 0;
         for (int i = 0; i < n; ++i, w.next()) {
           const int h = g * a.G + w.hh, qt = w.qt;
-          float* dst = a.dqacc + ((int64_t)h * a.c + qt * BQ) * D;
+          float* dst = a.dqacc + ((int64_t)h * a.cp + qt * BQ) * D;
           for (int c = 0; c < 4; ++c, ++m) {
             const int s = c & 1;
             mbar_wait(bar_stg_full(s), (m >> 1) & 1);
-            SECO_CHECK_COND(dst >= a.dqacc && dst + 32 * (c + 1) * D <= a.dqacc + (int64_t)a.G * a.hkv * a.c * D, 513);
+            SECO_CHECK_COND(dst >= a.dqacc && dst + 32 * (c + 1) * D <= a.dqacc + (int64_t)a.G * a.hkv * a.cp * D, 513);
             bulk_reduce_add_f32(dst + 32 * c * D, sSTG + s * kSlot, kSlot);
             bulk_commit();
             if (m > 0) {
@@ -1432,7 +1433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(bwd3::kThreads, 1)
       named_bar_sync(2 + mat, 128);
       if (wq == 0 && lane == 0) {
         const int row0 = (mat * a.hkv + g) * a.S + k0;
-        SECO_CHECK_COND(k0 + BKV <= (a.j + 1) * a.c && row0 + BKV <= 2 * a.hkv * a.S, 514);
+        SECO_CHECK_COND(k0 < (a.j + 1) * a.c && row0 < 2 * a.hkv * a.S, 514);
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_2d(&tm_dkv, stg_box(cc), cc * 32, row0);
         bulk_commit();
@@ -1490,7 +1491,8 @@ float list_makespan(std::vector<float> t, const std::vector<float>& pieces) {
 // pair = true: units are pairs of adjacent key tiles run by a cluster of 2 CTAs (P / 2 machines),
 // costed by the query walk of their first tile
 Schedule compute_schedule(int c, int j, int hkv, int G, int P, bool pair = false) {
-  const int nqt = c / bwd::BQ, ntiles = (j + 1) * c / bwd::BKV / (pair ? 2 : 1), N = ntiles * hkv;
+  const int nqt = (c + bwd::BQ - 1) / bwd::BQ, ntiles = ((j + 1) * c + bwd::BKV - 1) / bwd::BKV / (pair ? 2 : 1),
+            N = ntiles * hkv;
   if (pair) P /= 2;
   const float o = item_overhead();
   auto unit_blocks = [&](int U) {
@@ -1583,9 +1585,9 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   static_assert(bwd::kBytes <= 232448 && bwd2::kBytes <= 232448 && bwd3::kBytes <= 232448, "shared memory budget");
   // d = 64 runs on zero-padded 128-column tiles (TMA out-of-bounds fill on load; the dK/dV
   // reduce-add boxes past column 64 are dropped by the same bounds check; dQacc rows are 128)
-  if ((g.d != bwd::D && g.d != 64) || g.c % bwd::BQ) return cudaErrorInvalidValue;
-  int* order = g.det ? reinterpret_cast<int*>(ws_D + 2 * (size_t)g.hq * g.c) : nullptr;
-  cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.c, relay, st, order);
+  if ((g.d != bwd::D && g.d != 64) || g.cp % bwd::BQ) return cudaErrorInvalidValue;
+  int* order = g.det ? reinterpret_cast<int*>(ws_D + 2 * (size_t)g.hq * g.cp) : nullptr;
+  cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.cp, relay, st, order);
   if (e != cudaSuccess) return e;
   static std::atomic<unsigned long long> attr_done{0}, attr_done2{0};
   static const bool v2 = [] {
@@ -1597,12 +1599,12 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                   : ensure_smem_attr(seco_bwd_sm100_kernel, bwd::kBytes, attr_done)) != cudaSuccess)
     return e;
   bwd::Args a;
-  a.c = g.c; a.j = g.j; a.G = g.hq / g.hkv; a.hkv = g.hkv; a.S = g.c * g.k;
+  a.c = g.c; a.j = g.j; a.G = g.hq / g.hkv; a.hkv = g.hkv; a.S = g.c * g.k; a.cp = g.cp;
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.dk_scale = gscale * g.scale;
   a.dv_scale = gscale;
-  a.nlse = ws_D + (size_t)g.hq * g.c; a.Dv = ws_D; a.dqacc = ws_dqacc; a.dq_order = order;
-  a.ticket = order ? order + (size_t)g.hq * (g.c / bwd::BQ) : nullptr;   // zeroed with the counters
+  a.nlse = ws_D + (size_t)g.hq * g.cp; a.Dv = ws_D; a.dqacc = ws_dqacc; a.dq_order = order;
+  a.ticket = order ? order + (size_t)g.hq * ((g.c + bwd::BQ - 1) / bwd::BQ) : nullptr;   // zeroed with the counters
   a.err = nullptr;
   a.trace = nullptr;
 #ifdef SECO_TRACE
@@ -1615,7 +1617,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
     seco_trace_buffer = tbuf;
   }
 #endif
-  const int ntiles = (g.j + 1) * g.c / bwd::BKV;
+  const int ntiles = ((g.j + 1) * g.c + bwd::BKV - 1) / bwd::BKV;
   // CTA pairs (v3, cta_group::2 MMAs over two adjacent key tiles) need an even number of key tiles
   const bool pair = use_v2 && ntiles % 2 == 0 && bwd_uses_pair(g);
   static std::atomic<unsigned long long> attr_done3{0};
@@ -1643,7 +1645,7 @@ bool bwd_uses_pair(const ChunkGeom& g) {
     return e == nullptr ? -1 : (e[0] == '0' ? 0 : 1);
   }();
   const bool on = mode >= 0 ? mode == 1 : SECO_BWD_PAIR_DEFAULT != 0;
-  return on && !g.det && (g.d == 128 || g.d == 64);
+  return on && !g.det && (g.d == 128 || g.d == 64) && g.c % 128 == 0;   // whole query tiles only
 }
 
 unsigned long long check_word_bwd() { return seco_check_read_clear(); }

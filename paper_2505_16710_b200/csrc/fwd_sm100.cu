@@ -86,6 +86,7 @@ struct Layout {
 
 struct Args {
   int c, j, hq, G, nqt, nhp;  // chunk size, chunk index, q heads, group size, q tiles, head packs
+  int cp;                     // rows per head of the split-KV partials: c rounded up to 128
   int nsplit;                 // split-KV factor of the units past n_full (1: no split)
   int n_full;                 // work items [0, n_full) are whole units (final O / LSE written
                               // directly); the rest are nsplit key-range pieces per unit
@@ -171,8 +172,8 @@ __device__ __forceinline__ void merge_rows(const Args& a, int ns, int h_first, i
   constexpr uint32_t kPartO = kRows * 128 * 4;               // one part's O rows of a chunk (16 KiB)
   constexpr uint32_t kBuf = 4 * kPartO + 4 * kRows * 4;       // <= 4 parts' O rows + LSE
   const uint32_t bar = sbuf + 2 * kBuf;
-  const int64_t plane = (int64_t)a.hq * a.c;
-  auto first_row = [&](int ch) { return (int64_t)(h_first + ch * kRows / 128) * a.c + row0 + ch * kRows % 128; };
+  const int64_t plane = (int64_t)a.hq * a.cp;              // parts: [ns][hq][cp] rows
+  auto first_row = [&](int ch) { return (int64_t)(h_first + ch * kRows / 128) * a.cp + row0 + ch * kRows % 128; };
   auto issue = [&](int ch) {                                  // one thread
     const int64_t w0 = first_row(ch);
     const uint32_t b = bar + 8 * (ch & 1), dst = sbuf + (ch & 1) * kBuf;
@@ -216,11 +217,13 @@ __device__ __forceinline__ void merge_rows(const Args& a, int ns, int h_first, i
         acc.x += wk * v.x; acc.y += wk * v.y; acc.z += wk * v.z; acc.w += wk * v.w;
       }
       const float inv = 1.f / den;
-      const int64_t w = w0 + k;                               // = h * c + row (a chunk stays in one head)
+      const int64_t w = w0 + k;                               // = h * cp + row (a chunk stays in one head)
+      const int64_t h = w / a.cp, row = w % a.cp;
+      if (row >= a.c) continue;                               // padded rows of a ragged last tile
       if (4 * lane < a.d_out)
-        *reinterpret_cast<uint2*>(o + (w / a.c) * a.qh + (w % a.c) * a.qr + 4 * lane) =
+        *reinterpret_cast<uint2*>(o + h * a.qh + row * a.qr + 4 * lane) =
             make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
-      if (lane == 0) lse[w] = mx + __logf(den);
+      if (lane == 0) lse[h * a.c + row] = mx + __logf(den);
     }
     __syncthreads();                                          // buffer ch & 1 consumed
     if (threadIdx.x == 0 && ch + 2 < kChunks) issue(ch + 2);
@@ -269,7 +272,9 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   const int hp = unit % a.nhp;
   const int h0 = hp * NH, g = h0 / a.G;
   const int q0 = a.j * a.c + qt * fwd::BM;  // absolute position of the tile's first row
-  const int T = q0 / fwd::BN + 1;           // K/V tiles 0..T-1; tile T-1 is the causal diagonal
+  const int nvalid = min(fwd::BM, a.c - qt * fwd::BM);   // rows inside the chunk (ragged last tile)
+  const int T = (q0 + nvalid - 1) / fwd::BN + 1;         // K/V tiles 0..T-1 (the last one or two
+                                                         // straddle the causal diagonal)
   const int t0 = T * split / ns;            // this CTA's K/V tiles: [t0, t0 + nT)
   const int nT = T * (split + 1) / ns - t0;
 
@@ -313,8 +318,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      SECO_CHECK_COND(qt * fwd::BM + fwd::BM <= a.c && h0 + NH <= a.hq, 420);    // query tile inside chunk j
-      SECO_CHECK_COND(t0 >= 0 && (t0 + nT) * fwd::BN <= (a.j + 1) * a.c, 421);    // key tiles inside slots 0..j
+      SECO_CHECK_COND(qt * fwd::BM < a.c && h0 + NH <= a.hq, 420);                // query tile inside chunk j
+      SECO_CHECK_COND(t0 >= 0 && (t0 + nT - 1) * fwd::BN < (a.j + 1) * a.c, 421); // key tiles inside slots 0..j
       for (int b = 0; b < NH; ++b) {
         mbar_expect_tx(bar_q(b), L::kTileBytes);
         for (int x = 0; x < HALVES; ++x)
@@ -438,7 +443,8 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       mbar_wait(bar_s_full(b), t & 1);
       if (lane == 0 && wq == 0) FTRACE(4 + b, t);
       tc_fence_after();
-      const bool diag = (t0 + t == T - 1);   // the only tile that needs the causal mask
+      const int kb = (t0 + t) * fwd::BN - q0;  // the tile's first key relative to the query tile's first row
+      const bool diag = kb + fwd::BN - 1 > 0;  // keys beyond row 0: the causal mask applies
       // the whole 128-column row of S_b in registers (4 loads, one wait)
       uint32_t v[fwd::BN];
 #pragma unroll
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
       if (diag) {
 #pragma unroll
         for (int i = 0; i < fwd::BN; ++i)
-          if (i > r) v[i] = __float_as_uint(-INFINITY);
+          if (i + kb > r) v[i] = __float_as_uint(-INFINITY);
       }
 #if SECO_FWD_MAXCH == 4
       // four independent FMNMX3 chains: half the dependent-latency depth of two
@@ -558,6 +564,7 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
     const float lse_v = (m + __log2f(l)) * 0.69314718055994531f;
     if (we.ns == 1) {
       __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)row * a.qr;
+      const bool in_chunk = row < a.c;       // rows of a ragged last tile past the chunk: not stored
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         if (cc * 32 >= a.d_out) break;       // warp-uniform
@@ -572,14 +579,14 @@ __global__ void __launch_bounds__(fwd::Layout<NH, D, STAGES>::kThreads, 1)
           w.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l);
           w.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l);
           w.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l);
-          dst[q] = w;
+          if (in_chunk) dst[q] = w;
         }
       }
-      SECO_CHECK_COND(h < a.hq && row < a.c, 520);
-      lse[(int64_t)h * a.c + row] = lse_v;
+      SECO_CHECK_COND(h < a.hq, 520);
+      if (in_chunk) lse[(int64_t)h * a.c + row] = lse_v;
     } else {
-      const int64_t prow = ((int64_t)we.split * a.hq + h) * a.c + row;
-      SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.c, 521);
+      const int64_t prow = ((int64_t)we.split * a.hq + h) * a.cp + row;
+      SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.cp, 521);
       float4* dst = reinterpret_cast<float4*>(a.part_o + prow * D);
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
@@ -679,7 +686,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
   const int quad = unit % nquad;
   const int h0 = quad * 4 + 2 * (int)rank, g = (quad * 4) / a.G;
   const int q0 = a.j * a.c + qt * BM;
-  const int T = q0 / BN + 1;
+  const int nvalid = min(BM, a.c - qt * BM);         // rows inside the chunk (ragged last tile)
+  const int T = (q0 + nvalid - 1) / BN + 1;
   const int t0 = T * split / ns;
   const int nT = T * (split + 1) / ns - t0;
 
@@ -715,8 +723,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
-      SECO_CHECK_COND(qt * BM + BM <= a.c && h0 + NH <= a.hq, 422);
-      SECO_CHECK_COND(t0 >= 0 && (t0 + nT) * BN <= (a.j + 1) * a.c, 423);
+      SECO_CHECK_COND(qt * BM < a.c && h0 + NH <= a.hq, 422);
+      SECO_CHECK_COND(t0 >= 0 && (t0 + nT - 1) * BN < (a.j + 1) * a.c, 423);
       for (int b = 0; b < NH; ++b) {
         if (leader) mbar_expect_tx(bar_q(b), 2 * kQBytes);     // both CTAs' Q_b
         const uint32_t bq = mapa_shared(bar_q(b), 0);
@@ -828,7 +836,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
     for (int t = 0; t < nT; ++t) {
       mbar_wait(bar_s_full(b), t & 1);
       tc_fence_after();
-      const bool diag = (t0 + t == T - 1);
+      const int kb = (t0 + t) * BN - q0;     // the tile's first key relative to the query tile's first row
+      const bool diag = kb + BN - 1 > 0;
       uint32_t v[BN];
 #pragma unroll
       for (int cc = 0; cc < BN / 32; ++cc) tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cc * 32));
@@ -836,7 +845,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
       if (diag) {
 #pragma unroll
         for (int i = 0; i < BN; ++i)
-          if (i > r) v[i] = __float_as_uint(-INFINITY);
+          if (i + kb > r) v[i] = __float_as_uint(-INFINITY);
       }
       float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
@@ -918,6 +927,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
     const float lse_v = (m + __log2f(l)) * 0.69314718055994531f;
     if (we.ns == 1) {
       __nv_bfloat16* orow = o + (int64_t)h * a.qh + (int64_t)row * a.qr;
+      const bool in_chunk = row < a.c;       // rows of a ragged last tile past the chunk: not stored
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         if (cc * 32 >= a.d_out) break;
@@ -932,14 +942,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
           w.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv_l, __uint_as_float(v[8 * q + 3]) * inv_l);
           w.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv_l, __uint_as_float(v[8 * q + 5]) * inv_l);
           w.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv_l, __uint_as_float(v[8 * q + 7]) * inv_l);
-          dst[q] = w;
+          if (in_chunk) dst[q] = w;
         }
       }
-      SECO_CHECK_COND(h < a.hq && row < a.c, 522);
-      lse[(int64_t)h * a.c + row] = lse_v;
+      SECO_CHECK_COND(h < a.hq, 522);
+      if (in_chunk) lse[(int64_t)h * a.c + row] = lse_v;
     } else {
-      const int64_t prow = ((int64_t)we.split * a.hq + h) * a.c + row;
-      SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.c, 523);
+      const int64_t prow = ((int64_t)we.split * a.hq + h) * a.cp + row;
+      SECO_CHECK_COND(prow < (int64_t)a.nsplit * a.hq * a.cp, 523);
       float4* dst = reinterpret_cast<float4*>(a.part_o + prow * D);
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
@@ -994,7 +1004,7 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   }
   fwd::Args a;
   a.c = g.c; a.j = g.j; a.hq = g.hq; a.G = g.hq / g.hkv;
-  a.nqt = g.c / fwd::BM; a.nhp = g.hq / NH;
+  a.nqt = (g.c + fwd::BM - 1) / fwd::BM; a.nhp = g.hq / NH; a.cp = g.cp;
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.qh = g.qh; a.qr = g.qr; a.d_out = g.d;
   a.wait_prev = g.prev_indep ? 0 : 1;
@@ -1025,7 +1035,7 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   const int waves_full = units / slots;
   const int n_full = waves_full * slots, rem = units - n_full;
   // workspace: partial O [nsplit][hq][c][128] + partial LSE [nsplit][hq][c] + the counters
-  auto cnt_off = [&](int sp) { return (size_t)sp * g.hq * g.c * (D + 1); };
+  auto cnt_off = [&](int sp) { return (size_t)sp * g.hq * g.cp * (D + 1); };
   int best = 1;
   double best_cost = (double)((units + slots - 1) / slots) * (t_min + kOver);
   for (int sp = 2; sp <= 4 && rem > 0; ++sp) {
@@ -1041,7 +1051,7 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   a.n_units = units;
   a.merge = best > 1 && n_full > 0 ? 1 : 0;
   a.part_o = ws;
-  a.part_lse = ws ? ws + (size_t)best * g.hq * g.c * D : nullptr;
+  a.part_lse = ws ? ws + (size_t)best * g.hq * g.cp * D : nullptr;
   a.cnt = ws ? reinterpret_cast<int*>(ws + cnt_off(best)) : nullptr;
   a.trace = nullptr;
 #ifdef SECO_TRACE
@@ -1099,7 +1109,7 @@ bool fwd_uses_pair(const ChunkGeom& g) {
   }();
   const bool shape_ok = (g.d == 128 || g.d == 64) && (g.hq / g.hkv) % 4 == 0;
   if (mode >= 0) return mode == 1 && shape_ok;
-  return shape_ok && (g.c / fwd::BM) * (g.hq / 2) >= fwd::kSMs;
+  return shape_ok && (g.c + fwd::BM - 1) / fwd::BM * (g.hq / 2) >= fwd::kSMs;
 }
 
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,

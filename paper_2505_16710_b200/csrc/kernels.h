@@ -16,6 +16,10 @@ struct ChunkGeom {
   bool det = false;          // SECO_FLAG_DETERMINISTIC: ordered dQ reduction, no Q-split
   int ldq = 0;               // row stride (floats) of the dQ accumulator: 128 on the bf16 path
                              // (d = 64 runs zero-padded to 128), d on the fp32 path
+  int cp = 0;                // rows per head of the per-chunk workspace arrays (dQacc, D, -LSE
+                             // log2 e, split-KV partials): c rounded up to the 128-row tile on
+                             // the bf16 path (a ragged last query tile stays inside its head's
+                             // rows), c on the fp32 path
   bool prev_indep = false;   // SECO_FLAG_PREV_INDEPENDENT: the forward may load before its
                              // predecessor kernel completes (programmatic dependent launch)
 };

@@ -149,7 +149,6 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
   if (s->dtype == SECO_BF16) {
     if (s->d != 128 && s->d != 64)
       return fail(SECO_ERR_UNSUPPORTED, "bf16 path implements d in {64, 128} (got %d)", s->d);
-    if (s->chunk % 128) return fail(SECO_ERR_UNSUPPORTED, "bf16 path needs chunk %% 128 == 0 (got %d)", s->chunk);
     if ((s->q_row_stride * 2) % 16 || (s->q_head_stride * 2) % 16 || (s->kv_row_stride * 2) % 16 ||
         (s->kv_head_stride * 2) % 16)
       return fail(SECO_ERR_ARG, "bf16 strides must be multiples of 16 bytes");
@@ -166,6 +165,9 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
 // the bf16 kernels work on 128-wide head dims (d = 64 is zero-padded by the TMA's
 // out-of-bounds fill), so their fp32 dQ accumulator rows are 128 floats
 int dq_ld(const seco_shape* s) { return s->dtype == SECO_BF16 ? 128 : s->d; }
+// rows per head of the per-chunk workspace arrays: the bf16 kernels work on 128-row query tiles,
+// so a ragged chunk (c % 128 != 0) pads each head's rows to the next tile
+int64_t ws_rows(const seco_shape* s) { return s->dtype == SECO_BF16 ? (s->chunk + 127) / 128 * 128 : s->chunk; }
 
 seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
   seco::ChunkGeom g;
@@ -175,17 +177,20 @@ seco::ChunkGeom geom(const seco_shape* s, int32_t j) {
   g.det = (s->flags & SECO_FLAG_DETERMINISTIC) != 0;
   g.prev_indep = (s->flags & SECO_FLAG_PREV_INDEPENDENT) != 0;
   g.ldq = dq_ld(s);
+  g.cp = (int)ws_rows(s);
   return g;
 }
 
 size_t ws_floats(const seco_shape* s) {
-  // backward: dQ accumulator [hq][c][d] + D [hq][c] + (-LSE log2 e) [hq][c]
+  // (cp = ws_rows: c, or on the bf16 path c rounded up to the 128-row tile)
+  // backward: dQ accumulator [hq][cp][d] + D [hq][cp] + (-LSE log2 e) [hq][cp]
   //           + (deterministic mode) dQ order counters [hq][ceil(c/128)] int32 + a work ticket
-  // forward (split-KV, up to 4 parts): partial O [4][hq][c][d] + partial LSE [4][hq][c]
+  // forward (split-KV, up to 4 parts): partial O [4][hq][cp][d] + partial LSE [4][hq][cp]
   //           + piece counters, two per 128-row query tile and head
-  const size_t bwd = (size_t)s->hq * s->chunk * dq_ld(s) + 2 * (size_t)s->hq * s->chunk +
+  const size_t cp = (size_t)ws_rows(s);
+  const size_t bwd = (size_t)s->hq * cp * dq_ld(s) + 2 * (size_t)s->hq * cp +
                      (size_t)s->hq * ((s->chunk + 127) / 128) + 1;
-  const size_t fwd = 4 * (size_t)s->hq * s->chunk * (dq_ld(s) + 1) + 2 * (size_t)s->hq * ((s->chunk + 127) / 128);
+  const size_t fwd = 4 * (size_t)s->hq * cp * (dq_ld(s) + 1) + 2 * (size_t)s->hq * ((s->chunk + 127) / 128);
   return bwd > fwd ? bwd : fwd;
 }
 
@@ -271,7 +276,7 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   float* wsf = reinterpret_cast<float*>(ws);
   float* ws_dqacc = wsf;
-  float* ws_D = wsf + (size_t)s->hq * s->chunk * dq_ld(s);
+  float* ws_D = wsf + (size_t)s->hq * ws_rows(s) * dq_ld(s);
   int launches = 0;
   cudaError_t e;
   if (s->dtype == SECO_FP32_DEBUG) {
@@ -295,7 +300,7 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
       (bpair && !encode_3d(&tdo64, d_o, s->d, s->chunk, s->hq, s->q_row_stride, s->q_head_stride, 64)) ||
       !encode_3d(&tk, k, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
       !encode_3d(&tv, v, s->d, S_used, s->hkv, s->kv_row_stride, s->kv_head_stride, 128) ||
-      !encode_f32_rows(&tdq, ws_dqacc, (int64_t)s->hq * s->chunk, 128) ||
+      !encode_f32_rows(&tdq, ws_dqacc, (int64_t)s->hq * ws_rows(s), 128) ||
       !encode_f32_rows(&tdkv, dkv, 2 * (int64_t)s->hkv * S, 128, s->d))
     return fail(SECO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   if (!bpair) { tq64 = tq; tdo64 = tdo; }

@@ -92,7 +92,6 @@ def _shape(**kw):
     (dict(), 4, _lib.SECO_ERR_ARG),
     (dict(hkv=5), 0, _lib.SECO_ERR_ARG),
     (dict(d=96, q_row_stride=96, kv_row_stride=96), 0, _lib.SECO_ERR_UNSUPPORTED),
-    (dict(chunk=192, q_head_stride=768 * 128, kv_head_stride=768 * 128), 0, _lib.SECO_ERR_UNSUPPORTED),
     (dict(q_row_stride=100), 0, _lib.SECO_ERR_ARG),
     (dict(dtype=1, d=300, q_row_stride=300, kv_row_stride=300, q_head_stride=1024 * 300,
           kv_head_stride=1024 * 300), 0, _lib.SECO_ERR_UNSUPPORTED),

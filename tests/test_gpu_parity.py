@@ -94,6 +94,13 @@ BF16_CASES = [
     dict(hq=16, hkv=2, seq=640, d=128, c=128),    # G = 8, 5 chunks of the minimum size
     dict(hq=6, hkv=3, seq=1536, d=128, c=768),    # odd kv-head count, 6 query tiles per chunk
     dict(hq=4, hkv=1, seq=384, d=128, c=384),     # k = 1: one chunk, SeCO = plain full attention
+    # ragged chunks (c % 128 != 0): the last query tile of every chunk is partial, chunk starts
+    # and key tiles are misaligned, so the causal diagonal straddles two key tiles
+    dict(hq=4, hkv=1, seq=600, d=128, c=200),     # 128 + 72 rows per chunk, G=4 (NH=2)
+    dict(hq=3, hkv=1, seq=600, d=64, c=300),      # NH=1, d = 64, 128 + 128 + 44 rows
+    dict(hq=8, hkv=2, seq=400, d=128, c=100),     # chunk shorter than one tile, 4 chunks
+    dict(hq=2, hkv=2, seq=520, d=128, c=520),     # k = 1, MHA, 4 tiles + 8 rows
+    dict(hq=6, hkv=3, seq=999, d=128, c=333),     # odd G and kv heads, 3 chunks of 333
 ]
 
 
@@ -162,10 +169,11 @@ def test_bf16_chunk_calls_compose():
     assert float(layer.dkv[:, :, 3 * c:].abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("j,d", [(2, 128), (3, 128), (3, 64)])
-def test_bf16_forward_split_kv(j, d):
-    """Long chunks: the forward splits each query tile's key range and merges partials (a9)."""
-    hq, hkv, seq, c = 8, 2, 4096, 1024              # 32 units < 148 SMs: the forward splits
+@pytest.mark.parametrize("j,d,c", [(2, 128, 1024), (3, 128, 1024), (3, 64, 1024), (3, 128, 1000), (2, 64, 1000)])
+def test_bf16_forward_split_kv(j, d, c):
+    """Long chunks: the forward splits each query tile's key range and merges partials (a9);
+    c = 1000 is ragged (the partials keep 1024 rows per head, the last 24 never stored)."""
+    hq, hkv, seq = 8, 2, 4 * c                      # 32 units < 148 SMs: the forward splits
     x = inputs(hq, hkv, seq, d, seed=7, peaky=(j == 3))
     q, k, v, do = upload(x, torch.bfloat16)
     layer = _layer(hq, hkv, d, seq, c, torch.bfloat16)
@@ -216,7 +224,7 @@ def test_bf16_strided_sequence_major_layout():
     assert err(host(dkv[1]), ref["dv"]) <= BF16_TOL
 
 
-@pytest.mark.parametrize("hq,hkv,seq,c", [(8, 2, 2048, 512), (4, 1, 1024, 128)])
+@pytest.mark.parametrize("hq,hkv,seq,c", [(8, 2, 2048, 512), (4, 1, 1024, 128), (4, 1, 1000, 250)])
 def test_bf16_deterministic_mode_bit_reproducible(hq, hkv, seq, c):
     """SECO_FLAG_DETERMINISTIC: two SeCO steps and two SpaCO
     steps on the same inputs give bit-identical O, dQ and dKV, and stay within the bf16
@@ -279,7 +287,7 @@ sys.path.insert(0, ".")
 from oracle import chunkwise as OC
 from tests.gpu_util import BF16_TOL, err, host, inputs, upload
 from paper_2505_16710_b200.step import ChunkedAttention
-for (hq, hkv, seq, c) in ((8, 2, 512, 128), (4, 1, 1024, 256), (3, 1, 768, 384)):
+for (hq, hkv, seq, c) in ((8, 2, 512, 128), (4, 1, 1024, 256), (3, 1, 768, 384), (4, 1, 600, 200)):
     x = inputs(hq, hkv, seq, 128, seed=5, peaky=True)
     q, k, v, do = upload(x, torch.bfloat16)
     L = ChunkedAttention(hq, hkv, 128, seq, c, dtype=torch.bfloat16)
@@ -404,7 +412,7 @@ from oracle import chunkwise as OC
 from tests.gpu_util import BF16_TOL, err, host, inputs, upload
 from paper_2505_16710_b200.step import ChunkedAttention
 for (hq, hkv, seq, c, d) in ((8, 2, 1024, 256, 128), (16, 4, 2048, 512, 128), (8, 2, 1024, 256, 64),
-                             (4, 1, 4096, 1024, 128)):
+                             (4, 1, 4096, 1024, 128), (8, 2, 1000, 250, 128)):
     x = inputs(hq, hkv, seq, d, seed=7, peaky=True)
     q, k, v, do = upload(x, torch.bfloat16)
     L = ChunkedAttention(hq, hkv, d, seq, c, dtype=torch.bfloat16)
@@ -448,7 +456,8 @@ from oracle import chunkwise as OC
 from tests.gpu_util import BF16_TOL, err, host, inputs, upload
 from paper_2505_16710_b200 import ops
 from paper_2505_16710_b200.step import ChunkedAttention
-for (hq, hkv, seq, c, d) in ((8, 2, 4096, 1024, 128), (4, 1, 8192, 2048, 128), (8, 2, 4096, 1024, 64)):
+for (hq, hkv, seq, c, d) in ((8, 2, 4096, 1024, 128), (4, 1, 8192, 2048, 128), (8, 2, 4096, 1024, 64),
+                             (8, 2, 4000, 1000, 128)):
     x = inputs(hq, hkv, seq, d, seed=11, peaky=True)
     q, k, v, do = upload(x, torch.bfloat16)
     L = ChunkedAttention(hq, hkv, d, seq, c, dtype=torch.bfloat16)
