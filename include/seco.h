@@ -220,7 +220,7 @@ int32_t seco_last_launch_count(void);
  * G q-heads per kv-head and `num_sms` SMs (non-deterministic mode).  Writes
  * out4 = {n0, n1, f1, f2}: CTAs [0, n0) take whole 128-key units, the next n1 units
  * are split into f1 query-range pieces each, the rest into f2 pieces.
- * Returns the grid size.  chunk must be a multiple of 128. */
+ * Returns the grid size. */
 int32_t seco_debug_bwd_schedule(int32_t chunk, int32_t j, int32_t hkv, int32_t G, int32_t num_sms,
                                 int32_t* out4);
 
