@@ -45,8 +45,8 @@
  * validated on the host before any launch (SECO_ERR_ARG: null pointer, j out of
  * range, hq % hkv != 0, non-positive sizes, misaligned pointer or stride;
  * SECO_ERR_UNSUPPORTED: a shape the bf16 tensor-core path does not implement --
- * it needs d in {64, 128} (64 runs on zero-padded 128-wide tiles) and 16-byte
- * aligned rows; any chunk size c works (a ragged c % 128 != 0 leaves the last
+ * it needs d in {32, 64, 96, 128} (d < 128 runs on zero-padded 128-wide tiles)
+ * and 16-byte aligned rows; any chunk size c works (a ragged c % 128 != 0 leaves the last
  * query tile of each chunk partial: its rows past the chunk are zero-filled on
  * load, masked out of every softmax and never stored); the fp32 debug
  * path accepts any d <= 256 and any c).  Launch failures return SECO_ERR_CUDA;

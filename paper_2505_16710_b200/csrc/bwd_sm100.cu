@@ -1585,7 +1585,7 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   static_assert(bwd::kBytes <= 232448 && bwd2::kBytes <= 232448 && bwd3::kBytes <= 232448, "shared memory budget");
   // d = 64 runs on zero-padded 128-column tiles (TMA out-of-bounds fill on load; the dK/dV
   // reduce-add boxes past column 64 are dropped by the same bounds check; dQacc rows are 128)
-  if ((g.d != bwd::D && g.d != 64) || g.cp % bwd::BQ) return cudaErrorInvalidValue;
+  if (g.d > bwd::D || g.d % 32 || g.cp % bwd::BQ) return cudaErrorInvalidValue;
   int* order = g.det ? reinterpret_cast<int*>(ws_D + 2 * (size_t)g.hq * g.cp) : nullptr;
   cudaError_t e = launch_prep_bf16(g, o, d_o, ws_D, dkv, ws_dqacc, lse, ws_D + (size_t)g.hq * g.cp, relay, st, order);
   if (e != cudaSuccess) return e;
@@ -1645,7 +1645,7 @@ bool bwd_uses_pair(const ChunkGeom& g) {
     return e == nullptr ? -1 : (e[0] == '0' ? 0 : 1);
   }();
   const bool on = mode >= 0 ? mode == 1 : SECO_BWD_PAIR_DEFAULT != 0;
-  return on && !g.det && (g.d == 128 || g.d == 64) && g.c % 128 == 0;   // whole query tiles only
+  return on && !g.det && g.d <= 128 && g.d % 32 == 0 && g.c % 128 == 0;   // whole query tiles only
 }
 
 unsigned long long check_word_bwd() { return seco_check_read_clear(); }

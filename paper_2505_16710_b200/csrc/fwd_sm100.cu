@@ -1107,7 +1107,7 @@ bool fwd_uses_pair(const ChunkGeom& g) {
     const char* e = std::getenv("SECO_FWD_PAIR");
     return e == nullptr ? -1 : (e[0] == '0' ? 0 : 1);
   }();
-  const bool shape_ok = (g.d == 128 || g.d == 64) && (g.hq / g.hkv) % 4 == 0;
+  const bool shape_ok = g.d <= 128 && g.d % 32 == 0 && (g.hq / g.hkv) % 4 == 0;
   if (mode >= 0) return mode == 1 && shape_ok;
   return shape_ok && (g.c + fwd::BM - 1) / fwd::BM * (g.hq / 2) >= fwd::kSMs;
 }
@@ -1116,9 +1116,10 @@ cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              const CUtensorMap& tv, void* o, float* lse, float* ws, size_t ws_floats,
                              cudaStream_t st, int* launches) {
   const int G = g.hq / g.hkv;
-  // d = 64 runs the D = 128 kernel on zero-padded tiles: the tensor maps describe 64-column
-  // rows, so the TMA fills the second 64-column box of every tile with zeros
-  if (g.d == 128 || g.d == 64) {
+  // d = 32, 64, 96 run the D = 128 kernel on zero-padded tiles: the tensor maps describe
+  // d-column rows, so the TMA fills the columns past d with zeros (they add 0 to every dot
+  // product, and the epilogues store only the first d columns)
+  if (g.d <= 128 && g.d % 32 == 0) {
     // groups of 4 q-heads per kv head (LLaMA): CTA pairs over the 4 heads of a group, K / V
     // halves per CTA (tk must then have 64-row boxes: seco_api.cpp asks fwd_uses_pair)
     if (fwd_uses_pair(g)) return launch_fwd_impl<2, 128, 8, true>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);

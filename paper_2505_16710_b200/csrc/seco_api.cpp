@@ -147,8 +147,8 @@ seco_status check_shape(const seco_shape* s, int32_t j) {
       !disjoint(s->d, (int64_t)s->chunk * s->num_chunks, s->hkv, s->kv_row_stride, s->kv_head_stride))
     return fail(SECO_ERR_ARG, "strides overlap rows/heads (need head-major or row-major-interleaved rows)");
   if (s->dtype == SECO_BF16) {
-    if (s->d != 128 && s->d != 64)
-      return fail(SECO_ERR_UNSUPPORTED, "bf16 path implements d in {64, 128} (got %d)", s->d);
+    if (s->d > 128 || s->d % 32)
+      return fail(SECO_ERR_UNSUPPORTED, "bf16 path implements d in {32, 64, 96, 128} (got %d)", s->d);
     if ((s->q_row_stride * 2) % 16 || (s->q_head_stride * 2) % 16 || (s->kv_row_stride * 2) % 16 ||
         (s->kv_head_stride * 2) % 16)
       return fail(SECO_ERR_ARG, "bf16 strides must be multiples of 16 bytes");

@@ -91,7 +91,8 @@ def _shape(**kw):
     (dict(), -1, _lib.SECO_ERR_ARG),
     (dict(), 4, _lib.SECO_ERR_ARG),
     (dict(hkv=5), 0, _lib.SECO_ERR_ARG),
-    (dict(d=96, q_row_stride=96, kv_row_stride=96), 0, _lib.SECO_ERR_UNSUPPORTED),
+    (dict(d=80, q_row_stride=80, kv_row_stride=80, q_head_stride=1024 * 80, kv_head_stride=1024 * 80), 0,
+     _lib.SECO_ERR_UNSUPPORTED),                                              # bf16 needs d % 32 == 0
     (dict(q_row_stride=100), 0, _lib.SECO_ERR_ARG),
     (dict(dtype=1, d=300, q_row_stride=300, kv_row_stride=300, q_head_stride=1024 * 300,
           kv_head_stride=1024 * 300), 0, _lib.SECO_ERR_UNSUPPORTED),

@@ -37,7 +37,8 @@ def clean(what):
 
 cases = [(8, 2, 512, 128, 128, False), (3, 1, 768, 128, 384, False), (8, 2, 512, 64, 128, False),
          (6, 3, 1536, 128, 768, False), (8, 2, 4096, 128, 1024, False), (4, 1, 1024, 128, 256, True),
-         (4, 1, 600, 128, 200, False), (8, 2, 4000, 128, 1000, False), (4, 1, 1000, 128, 250, True)]
+         (4, 1, 600, 128, 200, False), (8, 2, 4000, 128, 1000, False), (4, 1, 1000, 128, 250, True),
+         (4, 1, 512, 96, 256, False), (8, 2, 600, 32, 200, False)]
 for hq, hkv, seq, d, c, det in cases:
     x = inputs(hq, hkv, seq, d, seed=9, peaky=True)
     q, k, v, do = upload(x, torch.bfloat16)

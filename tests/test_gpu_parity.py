@@ -101,6 +101,8 @@ BF16_CASES = [
     dict(hq=8, hkv=2, seq=400, d=128, c=100),     # chunk shorter than one tile, 4 chunks
     dict(hq=2, hkv=2, seq=520, d=128, c=520),     # k = 1, MHA, 4 tiles + 8 rows
     dict(hq=6, hkv=3, seq=999, d=128, c=333),     # odd G and kv heads, 3 chunks of 333
+    dict(hq=4, hkv=1, seq=512, d=96, c=256),      # d = 96 (zero-padded to the 128-wide tiles)
+    dict(hq=8, hkv=2, seq=600, d=32, c=200),      # d = 32, ragged chunks
     dict(hq=2, hkv=1, seq=5, d=128, c=1),         # degenerate: 1-token chunks (every row its own chunk)
     dict(hq=4, hkv=2, seq=21, d=64, c=7),         # 7-token chunks, d = 64
 ]
