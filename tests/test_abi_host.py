@@ -91,6 +91,10 @@ def _shape(**kw):
     (dict(), -1, _lib.SECO_ERR_ARG),
     (dict(), 4, _lib.SECO_ERR_ARG),
     (dict(hkv=5), 0, _lib.SECO_ERR_ARG),
+    (dict(chunk=0), 0, _lib.SECO_ERR_ARG),                                   # empty chunk
+    (dict(num_chunks=0), 0, _lib.SECO_ERR_ARG),                              # empty sequence
+    (dict(hq=0), 0, _lib.SECO_ERR_ARG),                                      # no heads
+    (dict(d=0), 0, _lib.SECO_ERR_ARG),                                       # empty head dim
     (dict(d=80, q_row_stride=80, kv_row_stride=80, q_head_stride=1024 * 80, kv_head_stride=1024 * 80), 0,
      _lib.SECO_ERR_UNSUPPORTED),                                              # bf16 needs d % 32 == 0
     (dict(q_row_stride=100), 0, _lib.SECO_ERR_ARG),
