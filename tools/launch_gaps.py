@@ -25,7 +25,7 @@ SHAPES = {"cfg3": (32, 8, 128, 32768, 2048), "cfg3r8": (4, 1, 128, 32768, 2048),
 
 
 def short(name):
-    for key in ("seco_fwd_sm100", "seco_bwd2_sm100", "seco_bwd_sm100", "bwd_prep", "bwd_final", "fwd_combine",
+    for key in ("seco_fwd_sm100", "seco_fwd2_sm100", "seco_bwd2_sm100", "seco_bwd_sm100", "bwd_prep", "bwd_final", "fwd_combine",
                 "chunk_skip"):
         if key in name:
             return key
@@ -55,6 +55,9 @@ def run(cfg):
     print(f"   span {span:.1f} us, kernels busy {busy:.1f} us, gaps {sum(gaps):.1f} us "
           f"({100 * sum(gaps) / span:.2f}% of the step); gap median {statistics.median(gaps):.2f} us, "
           f"max {max(gaps):.2f} us (overlapping PDL launches count as 0)")
+    if os.environ.get("GAPS_DETAIL"):                # every launch: kernel, duration, gap before it
+        for e, gp in zip(ks, [0.0] + gaps):
+            print(f"     {short(e['name']):18s} {e['dur']:9.1f} us  gap before {gp:6.2f} us")
     by = {}
     for e, gp in zip(ks, [0.0] + gaps):
         n = short(e["name"])
