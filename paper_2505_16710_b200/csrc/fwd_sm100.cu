@@ -25,6 +25,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef SECO_FWD_PAIR_STAGES
+#define SECO_FWD_PAIR_STAGES 8   // K / V half-tile ring slots of the pair kernel (16 KiB each)
+#endif
+
 namespace seco {
 
 #ifdef SECO_TRACE
@@ -1122,7 +1126,8 @@ cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
   if (g.d <= 128 && g.d % 32 == 0) {
     // groups of 4 q-heads per kv head (LLaMA): CTA pairs over the 4 heads of a group, K / V
     // halves per CTA (tk must then have 64-row boxes: seco_api.cpp asks fwd_uses_pair)
-    if (fwd_uses_pair(g)) return launch_fwd_impl<2, 128, 8, true>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
+    if (fwd_uses_pair(g))
+      return launch_fwd_impl<2, 128, SECO_FWD_PAIR_STAGES, true>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
     if (G % 2 == 0) return launch_fwd_impl<2, 128, 5, false>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
     return launch_fwd_impl<1, 128, 6, false>(g, tq, tk, tv, o, lse, ws, ws_floats, st, launches);
   }
