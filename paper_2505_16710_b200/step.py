@@ -117,7 +117,13 @@ class ChunkedAttention:
         """Issue a plan on one stream (the checkpoint gradients start at zero: dkv is zeroed
         first).  events: optional per-call (start, end) CUDA event pairs; nvtx: one NVTX range
         per chunk call (for a profiler timeline).  Returns the number of kernel launches."""
-        self.dkv.zero_()          # checkpoint grads m'.grad start at zero each step (caller-owned buffer)
+        # checkpoint grads m'.grad start at zero each step (caller-owned buffer), zeroed on the
+        # stream the chunk calls go to
+        if stream is None:
+            self.dkv.zero_()
+        else:
+            with torch.cuda.stream(stream):
+                self.dkv.zero_()
         launches = 0
         for n, op in enumerate(order):
             if nvtx:
