@@ -63,9 +63,9 @@ def test_fp32_seco_stack_matches_full_gradient(L, hq, hkv, d, hd, S, c):
     assert model.reducer.sent == list(reversed(range(L)))   # buckets final top-down on the last chunk
 
 
-@pytest.mark.parametrize("d", [64, 128])
-def test_bf16_seco_stack_matches_full_gradient(d):
-    L, hq, hkv, hd, S, c = 2, 4, 2, 128, 512, 128
+@pytest.mark.parametrize("d,S,c", [(64, 512, 128), (128, 512, 128), (128, 600, 200)])
+def test_bf16_seco_stack_matches_full_gradient(d, S, c):
+    L, hq, hkv, hd = 2, 4, 2, 128                    # c = 200: ragged chunks through the stack
     inp = make_stack_inputs(L, hd, hq, hkv, d, 8, S, seed=11, bf16=True)
     model = _stack(inp, hq, hkv, d, S, c, torch.bfloat16)
     x0, G = _inputs(inp, torch.bfloat16)
