@@ -40,7 +40,13 @@ def _stream(stream):
 
 
 def _p(t):
-    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+    """Device pointer of a CUDA tensor (NULL for None).  A host tensor is refused here: the
+    library takes device pointers and would only fault at the next synchronisation."""
+    if t is None:
+        return ctypes.c_void_p(0)
+    if not t.is_cuda:
+        raise ValueError("libseco takes CUDA tensors (got a tensor on %s)" % t.device)
+    return ctypes.c_void_p(t.data_ptr())
 
 
 def chunk_view(t: torch.Tensor, shape: SecoShape, j: int) -> torch.Tensor:

@@ -226,3 +226,16 @@ def test_bwd_work_list_covers_every_block_once(lib, c, k, hkv, G):
 def test_normal_build_has_no_checks(lib):
     """The product libseco.so is not the bounds-checked build (tests/test_gpu_check.py runs that)."""
     assert lib.seco_debug_check_enabled() == 0
+
+
+def test_binding_refuses_host_tensors():
+    """The binding passes device pointers only: a host tensor is refused before the library
+    is called (it would otherwise fault on the device at the next synchronisation)."""
+    import torch
+    from paper_2505_16710_b200 import ops
+    q = torch.zeros(2, 256, 128, dtype=torch.bfloat16)
+    k = torch.zeros(1, 256, 128, dtype=torch.bfloat16)
+    shape = ops.make_shape(q, k, 128)
+    lse = torch.zeros(2, 128)
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        ops.seco_chunk_forward(shape, 0, q[:, :128], k, k, q[:, :128], lse)
