@@ -12,6 +12,21 @@
 #include "common.cuh"
 #include "kernels.h"
 
+// Grid sizes of the memory-bound helpers for large chunk calls (>= kBigRows query rows; smaller
+// calls keep 296 blocks, which measured faster on the 8-rank per-rank shape): multiples of the
+// 148 SMs, measured at cfg3 with tools/launch_gaps.py: prep 17.2 -> 14.0 us,
+// final 13.4 -> 10.7 us against 296 blocks and 4 rows in flight
+#ifndef SECO_FINAL_U
+#define SECO_FINAL_U 8          // bwd_final, d = 128: rows in flight per thread
+#endif
+#ifndef SECO_FINAL_BLOCKS
+#define SECO_FINAL_BLOCKS 592   // bwd_final dQ blocks (4 per SM)
+#endif
+#ifndef SECO_PREP_BLOCKS
+#define SECO_PREP_BLOCKS 888    // bwd_prep blocks per task (D rows; dQacc zeroing), 6 per SM
+#endif
+constexpr int kBigRows = 32768;  // hq * c
+
 namespace seco {
 
 template <typename T> SECO_DEV float ldf(const T* p);
@@ -170,10 +185,10 @@ __global__ void __launch_bounds__(256) bwd_final_kernel(const float* __restrict_
   if (bid < a.nQ) {
     if (dqacc == nullptr) return;
     if (dv4 == 32) {
-      // d = 128: one float4 per (row, lane); a thread keeps 4 rows' loads in flight before its
+      // d = 128: one float4 per (row, lane); a thread keeps U rows' loads in flight before its
       // stores (32-bit index math: row = idx >> 5)
       const int rows = a.hq * a.c, total = rows * 32, stride = a.nQ * (int)blockDim.x;
-      constexpr int U = 4;
+      constexpr int U = SECO_FINAL_U;
       for (int base = bid * (int)blockDim.x + (int)threadIdx.x; base < total; base += U * stride) {
         float4 v[U];
 #pragma unroll
@@ -265,9 +280,10 @@ static cudaError_t launch_prep(const ChunkGeom& g, const T* o, const T* d_o, flo
   a.cp = g.cp > 0 ? g.cp : g.c;
   a.qh = g.qh; a.qr = g.qr; a.relay = relay;
   a.vec = (sizeof(T) == 2 && (g.d == 64 || g.d == 128)) ? 1 : 0;
-  a.nD = a.vec ? 296 : (g.hq * g.c + 7) / 8;
+  const int blocks = g.hq * g.c >= kBigRows ? SECO_PREP_BLOCKS : 296;
+  a.nD = a.vec ? blocks : (g.hq * g.c + 7) / 8;
   a.nR = relay == 1.f ? 0 : 296;
-  a.nZ = dqacc ? 296 : 0;
+  a.nZ = dqacc ? blocks : 0;
   a.order = order;
   a.ldq = g.ldq ? g.ldq : g.d;
   a.n_order = g.hq * ((g.c + 127) / 128) + 1;   // order counters + the deterministic-mode work ticket
@@ -282,7 +298,7 @@ static cudaError_t launch_final(const ChunkGeom& g, const float* dqacc, T* dq, c
   a.hq = g.hq; a.hkv = g.hkv; a.c = g.c; a.d = g.d; a.j = g.j; a.S = g.c * g.k;
   a.qh = g.qh; a.qr = g.qr; a.dq_scale = dq_scale; a.ldq = g.ldq ? g.ldq : g.d;
   a.cp = g.cp > 0 ? g.cp : g.c;
-  a.nQ = dqacc ? 296 : 0;
+  a.nQ = dqacc ? (g.hq * g.c >= kBigRows ? SECO_FINAL_BLOCKS : 296) : 0;
   a.nO = (dk_own || dv_own) ? 148 : 0;
   if (a.nQ + a.nO == 0) return cudaSuccess;
   bwd_final_kernel<T><<<a.nQ + a.nO, 256, 0, st>>>(dqacc, dq, dkv, dk_own, dv_own, a);
