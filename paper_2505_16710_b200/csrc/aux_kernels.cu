@@ -415,15 +415,26 @@ __global__ void __launch_bounds__(256) fwd_combine_kernel(const float* __restric
   if (w >= a.hq * a.c) return;
   const int h = w / a.c, r = w % a.c;
   const int64_t plane = (int64_t)a.hq * a.cp, pw = (int64_t)h * a.cp + r;   // partial row
+  // every part's LSE and O slice requested before any is used (nsplit <= 4)
+  float lp[4];
+  float4 v[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    lp[s] = s < a.nsplit ? part_lse[s * plane + pw] : -INFINITY;
+    v[s] = s < a.nsplit ? reinterpret_cast<const float4*>(part_o + (s * plane + pw) * 128)[lane]
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float mx = -INFINITY;
-  for (int s = 0; s < a.nsplit; ++s) mx = fmaxf(mx, part_lse[s * plane + pw]);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) mx = fmaxf(mx, lp[s]);
   float den = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s = 0; s < a.nsplit; ++s) {
-    const float wt = __expf(part_lse[s * plane + pw] - mx);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s >= a.nsplit) break;
+    const float wt = __expf(lp[s] - mx);
     den += wt;
-    const float4 v = reinterpret_cast<const float4*>(part_o + (s * plane + pw) * 128)[lane];
-    acc.x += wt * v.x; acc.y += wt * v.y; acc.z += wt * v.z; acc.w += wt * v.w;
+    acc.x += wt * v[s].x; acc.y += wt * v[s].y; acc.z += wt * v[s].z; acc.w += wt * v[s].w;
   }
   const float inv = 1.f / den;
   if (4 * lane >= a.d) { if (lane == 0) lse[w] = mx + __logf(den); return; }
