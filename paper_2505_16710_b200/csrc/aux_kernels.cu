@@ -120,14 +120,24 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const T* __restrict__ o, 
     if (a.relay == 1.f) return;
     const int64_t per = (int64_t)a.c * a.d;                 // one slot of one head
     const int64_t total = 2 * (int64_t)a.hkv * per / 4;     // float4 units
-    for (int64_t i = (int64_t)(bid - a.nD) * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)a.nR * blockDim.x) {
-      const int64_t e = i * 4;
-      const int64_t th = e / per, off = e % per;              // th = tensor*hkv + g
-      float4* p = reinterpret_cast<float4*>(dkv + th * (int64_t)a.S * a.d + (int64_t)a.j * per + off);
-      float4 v = *p;
-      v.x *= a.relay; v.y *= a.relay; v.z *= a.relay; v.w *= a.relay;
-      *p = v;
+    const int64_t stride = (int64_t)a.nR * blockDim.x;
+    constexpr int U = 4;                                    // float4s in flight per thread
+    for (int64_t i0 = (int64_t)(bid - a.nD) * blockDim.x + threadIdx.x; i0 < total; i0 += U * stride) {
+      float4* p[U];
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride, e = (i < total ? i : 0) * 4;
+        const int64_t th = e / per, off = e % per;            // th = tensor*hkv + g
+        p[u] = reinterpret_cast<float4*>(dkv + th * (int64_t)a.S * a.d + (int64_t)a.j * per + off);
+        if (i < total) v[u] = *p[u];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u * stride >= total) break;
+        v[u].x *= a.relay; v[u].y *= a.relay; v[u].z *= a.relay; v[u].w *= a.relay;
+        *p[u] = v[u];
+      }
     }
   } else {
     if (bid == a.nD + a.nR) {
