@@ -188,7 +188,7 @@ def _bwd_work_list(lib, c, j, hkv, G, sms):
     out = (ctypes.c_int32 * 4)()
     grid = lib.seco_debug_bwd_schedule(c, j, hkv, G, sms, out)
     n0, n1, f1, f2 = list(out)
-    nqt, ntiles = c // 128, (j + 1) * c // 128
+    nqt, ntiles = -(-c // 128), -(-(j + 1) * c // 128)        # ceil: ragged chunks (c % 128 != 0)
     ranges = {}
     for bid in range(grid):
         if bid < n0:
@@ -207,7 +207,8 @@ def _bwd_work_list(lib, c, j, hkv, G, sms):
 
 
 @pytest.mark.parametrize("c,k,hkv,G", [(2048, 16, 8, 4), (1024, 8, 8, 4), (4096, 32, 1, 4), (1024, 16, 2, 4),
-                                       (256, 5, 3, 2), (128, 4, 1, 1)])
+                                       (256, 5, 3, 2), (128, 4, 1, 1),
+                                       (200, 3, 2, 2), (1000, 4, 8, 4), (100, 4, 1, 4)])   # ragged chunks
 def test_bwd_work_list_covers_every_block_once(lib, c, k, hkv, G):
     """The balanced backward work list (whole units, then f1- / f2-way query splits for the
     last wave): every (key tile, kv head) unit appears, its pieces tile [0, n_all) exactly,
