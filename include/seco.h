@@ -224,6 +224,13 @@ int32_t seco_last_launch_count(void);
 int32_t seco_debug_bwd_schedule(int32_t chunk, int32_t j, int32_t hkv, int32_t G, int32_t num_sms,
                                 int32_t* out4);
 
+/* Debug / test hook: the work plan seco_chunk_forward(shape, j) uses with a workspace of
+ * seco_workspace_size(shape) bytes on a GPU with num_sms SMs (<= 0: this library's 148),
+ * host only, bf16 shapes.  out5 = {CTA-pair kernel (0/1), work units, whole units n_full,
+ * key-range pieces per split unit (1: no split), in-kernel merge (1) or combine kernel (0)}.
+ * Returns the grid size in CTAs, -1 for an invalid shape. */
+int32_t seco_debug_fwd_schedule(const seco_shape* shape, int32_t j, int32_t num_sms, int32_t* out5);
+
 /* Bounds-check builds (libseco_check.so, compiled with -DSECO_CHECK=1; the stand-in for
  * compute-sanitizer, which this GPU pool does not offer).  Every kernel asserts its shared-
  * and tensor-memory operand ranges, mbarrier alignment, TMA box coordinates and global store

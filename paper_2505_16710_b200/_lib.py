@@ -17,6 +17,7 @@ EXPORTS = ("seco_workspace_size", "seco_chunk_forward", "seco_chunk_backward", "
            "spaco_sample_and_scale",
            "seco_lora_workspace_size", "seco_lora_grad",
            "seco_status_string", "seco_last_error", "seco_last_launch_count", "seco_debug_bwd_schedule",
+           "seco_debug_fwd_schedule",
            "seco_debug_check_enabled", "seco_debug_check_word", "seco_debug_check_selftest")
 
 
@@ -88,6 +89,9 @@ def load():
     if hasattr(lib, "seco_debug_bwd_schedule"):      # (older experiment variants lack it)
         lib.seco_debug_bwd_schedule.argtypes = [i32, i32, i32, i32, i32, P(i32)]
         lib.seco_debug_bwd_schedule.restype = i32
+    if hasattr(lib, "seco_debug_fwd_schedule"):
+        lib.seco_debug_fwd_schedule.argtypes = [P(SecoShape), i32, i32, P(i32)]
+        lib.seco_debug_fwd_schedule.restype = i32
     _lib = lib
     return lib
 

@@ -987,6 +987,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fwd2::Layout<STAGES>
 #endif
 }
 
+namespace fwd {
+// float offset of the split-KV piece counters in the workspace: after the partial O
+// [sp][hq][cp][128] and partial LSE [sp][hq][cp]
+inline size_t split_counter_offset(const ChunkGeom& g, int sp) { return (size_t)sp * g.hq * g.cp * (128 + 1); }
+
+// Split-KV plan of one forward call (§8 row a9).  A sub-wave grid (fewer units than work slots:
+// head-sharded ranks, short chunks) cuts every unit into nsplit key ranges and merges the parts
+// with the combine kernel.  A multi-wave grid runs DP + split tail: the first n_full units (as
+// many whole waves as the grid fills) run whole, the remaining ones are cut into nsplit key
+// ranges whose pieces fill the last waves, and the piece that finishes a unit last merges its
+// parts in-kernel (there the merges overlap other pieces' work; in a sub-wave grid every merge
+// would sit on the critical path, where the combine kernel spreads it over all SMs).  Cost in
+// K/V-tile times per work slot (an SM, or a cluster for the pair kernel): kOver tiles of
+// prologue / epilogue per CTA; the combine ~0.15 of a unit; kMerge per round of pieces for the
+// partial rows and the in-kernel merge (measured).  SECO_FWD_NSPLIT=s forces s;
+// SECO_FWD_SLOTS=n pretends n SMs (tests reach the DP + tail form on small shapes).
+struct SplitPlan {
+  int units, n_full, nsplit, merge;
+  int items() const { return n_full + (units - n_full) * nsplit; }
+};
+inline SplitPlan split_plan(const ChunkGeom& g, int units, bool pair, bool have_ws, size_t ws_floats,
+                            int sms = 0) {
+  constexpr double kOver = 8.0, kMerge = 7.0;
+  static const int forced = [] {
+    const char* e = std::getenv("SECO_FWD_NSPLIT");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
+  static const int slots_env = [] {
+    const char* e = std::getenv("SECO_FWD_SLOTS");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
+  const int sm_slots = sms > 0 ? sms : slots_env > 0 ? slots_env : kSMs;
+  const int slots = pair ? (sm_slots + 1) / 2 : sm_slots;
+  const int t_min = g.j * g.c / BN + 1;                // K/V tiles of the lightest unit
+  const int waves_full = units / slots;
+  const int n_full = waves_full * slots, rem = units - n_full;
+  int best = 1;
+  double best_cost = (double)((units + slots - 1) / slots) * (t_min + kOver);
+  for (int sp = 2; sp <= 4 && rem > 0; ++sp) {
+    if (t_min < 8 * sp || g.j == 0 || !have_ws || split_counter_offset(g, sp) + (size_t)2 * units > ws_floats) break;
+    const int rounds = (rem * sp + slots - 1) / slots;
+    const double cost = waves_full * (t_min + kOver) + rounds * ((double)t_min / sp + kOver) +
+                        (waves_full == 0 ? 0.15 * t_min : kMerge * rounds);
+    if (forced ? sp == forced : cost < best_cost) { best_cost = cost; best = sp; }
+  }
+  if (forced == 1) best = 1;
+  return SplitPlan{units, best > 1 ? n_full : units, best, best > 1 && n_full > 0 ? 1 : 0};
+}
+}  // namespace fwd
+
 cudaError_t launch_fwd_combine(const ChunkGeom& g, int nsplit, const float* part_o, const float* part_lse, void* o,
                                float* lse, cudaStream_t st);
 
@@ -1012,48 +1062,13 @@ static cudaError_t launch_fwd_impl(const ChunkGeom& g, const CUtensorMap& tq, co
   a.scale_log2 = g.scale * 1.4426950408889634f;
   a.qh = g.qh; a.qr = g.qr; a.d_out = g.d;
   a.wait_prev = g.prev_indep ? 0 : 1;
-  // split-KV (§8 row a9).  A sub-wave grid (fewer units than work slots: head-sharded ranks,
-  // short chunks) cuts every unit into nsplit key ranges and merges the parts with the combine
-  // kernel.  A multi-wave grid runs DP + split tail: the first n_full units (as many whole waves
-  // as the grid fills) run whole, the remaining ones are cut into nsplit key ranges whose
-  // pieces fill the last waves, and the piece that finishes a unit last merges its parts
-  // in-kernel (there the merges overlap other pieces' work; in a sub-wave grid every merge
-  // would sit on the critical path, where the combine kernel spreads it over all SMs).  Cost
-  // in K/V-tile times per work slot (an SM, or a cluster for the pair kernel): kOver tiles of
-  // prologue / epilogue per CTA; the combine ~0.15 of a unit; kMerge per round of pieces for
-  // the partial rows and the in-kernel merge (measured).  SECO_FWD_NSPLIT=s forces
-  // s; SECO_FWD_SLOTS=n pretends n work slots (tests reach the DP + tail form on small shapes).
-  constexpr double kOver = 8.0, kMerge = 7.0;
-  static const int forced = [] {
-    const char* e = std::getenv("SECO_FWD_NSPLIT");
-    return e == nullptr ? 0 : std::atoi(e);
-  }();
-  static const int slots_env = [] {
-    const char* e = std::getenv("SECO_FWD_SLOTS");
-    return e == nullptr ? 0 : std::atoi(e);
-  }();
-  const int units = a.nqt * a.nhp / (PAIR ? 2 : 1);   // work units (pairs: 4-head quads)
-  const int sm_slots = slots_env > 0 ? slots_env : fwd::kSMs;
-  const int slots = PAIR ? (sm_slots + 1) / 2 : sm_slots;
-  const int t_min = g.j * g.c / fwd::BN + 1;          // K/V tiles of the lightest unit
-  const int waves_full = units / slots;
-  const int n_full = waves_full * slots, rem = units - n_full;
-  // workspace: partial O [nsplit][hq][c][128] + partial LSE [nsplit][hq][c] + the counters
-  auto cnt_off = [&](int sp) { return (size_t)sp * g.hq * g.cp * (D + 1); };
-  int best = 1;
-  double best_cost = (double)((units + slots - 1) / slots) * (t_min + kOver);
-  for (int sp = 2; sp <= 4 && rem > 0; ++sp) {
-    if (t_min < 8 * sp || g.j == 0 || ws == nullptr || cnt_off(sp) + (size_t)2 * units > ws_floats) break;
-    const int rounds = (rem * sp + slots - 1) / slots;
-    const double cost = waves_full * (t_min + kOver) + rounds * ((double)t_min / sp + kOver) +
-                        (waves_full == 0 ? 0.15 * t_min : kMerge * rounds);
-    if (forced ? sp == forced : cost < best_cost) { best_cost = cost; best = sp; }
-  }
-  if (forced == 1) best = 1;
+  const fwd::SplitPlan pl = fwd::split_plan(g, a.nqt * a.nhp / (PAIR ? 2 : 1), PAIR, ws != nullptr, ws_floats);
+  const int units = pl.units, best = pl.nsplit;
   a.nsplit = best;
-  a.n_full = best > 1 ? n_full : units;
+  a.n_full = pl.n_full;
   a.n_units = units;
-  a.merge = best > 1 && n_full > 0 ? 1 : 0;
+  a.merge = pl.merge;
+  auto cnt_off = [&](int sp) { return fwd::split_counter_offset(g, sp); };
   a.part_o = ws;
   a.part_lse = ws ? ws + (size_t)best * g.hq * g.cp * D : nullptr;
   a.cnt = ws ? reinterpret_cast<int*>(ws + cnt_off(best)) : nullptr;
@@ -1114,6 +1129,15 @@ bool fwd_uses_pair(const ChunkGeom& g) {
   const bool shape_ok = g.d <= 128 && g.d % 32 == 0 && (g.hq / g.hkv) % 4 == 0;
   if (mode >= 0) return mode == 1 && shape_ok;
   return shape_ok && (g.c + fwd::BM - 1) / fwd::BM * (g.hq / 2) >= fwd::kSMs;
+}
+
+int32_t fwd_debug_plan(const ChunkGeom& g, size_t ws_floats, int sms, int32_t* out5) {
+  const bool pair = fwd_uses_pair(g);
+  const int NH = pair || (g.hq / g.hkv) % 2 == 0 ? 2 : 1;
+  const int nqt = (g.c + fwd::BM - 1) / fwd::BM;
+  const fwd::SplitPlan pl = fwd::split_plan(g, nqt * (g.hq / NH) / (pair ? 2 : 1), pair, true, ws_floats, sms);
+  out5[0] = pair ? 1 : 0; out5[1] = pl.units; out5[2] = pl.n_full; out5[3] = pl.nsplit; out5[4] = pl.merge;
+  return pl.items() * (pair ? 2 : 1);
 }
 
 cudaError_t launch_fwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CUtensorMap& tk,

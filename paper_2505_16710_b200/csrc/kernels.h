@@ -58,6 +58,10 @@ cudaError_t launch_bwd_sm100(const ChunkGeom& g, const CUtensorMap& tq, const CU
                              void* dk_own, void* dv_own, float* ws_dqacc, float* ws_D, cudaStream_t st,
                              int* launches);
 
+// the forward's work plan for a call (seco_debug_fwd_schedule): out5 = {pair kernel, units,
+// whole units n_full, pieces per split unit, in-kernel merge}; returns the grid size in CTAs
+int32_t fwd_debug_plan(const ChunkGeom& g, size_t ws_floats, int sms, int32_t* out5);
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device), thread-safe:
 // `done` holds one bit per device ordinal (the attribute is per device).
 template <typename Kernel>

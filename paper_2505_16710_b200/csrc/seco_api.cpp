@@ -311,6 +311,11 @@ seco_status seco_chunk_backward(const seco_shape* s, int32_t j, const void* q, c
   return SECO_OK;
 }
 
+int32_t seco_debug_fwd_schedule(const seco_shape* s, int32_t j, int32_t num_sms, int32_t* out5) {
+  if (check_shape(s, j) != SECO_OK || s->dtype != SECO_BF16 || !out5) return -1;
+  return seco::fwd_debug_plan(geom(s, j), ws_floats(s), num_sms, out5);
+}
+
 seco_status spaco_chunk_skip(const seco_shape* s, int32_t j, float* dkv, void* dq, void* dk_own, void* dv_own,
                              seco_stream_t stream) {
   g_launches = 0;

@@ -240,3 +240,41 @@ def test_binding_refuses_host_tensors():
     lse = torch.zeros(2, 128)
     with pytest.raises(ValueError, match="CUDA tensors"):
         ops.seco_chunk_forward(shape, 0, q[:, :128], k, k, q[:, :128], lse)
+
+
+def _fwd_plan(lib, hq, hkv, c, k, j, sms=0):
+    s = _shape(hq=hq, hkv=hkv, chunk=c, num_chunks=k, q_head_stride=k * c * 128, kv_head_stride=k * c * 128)
+    out = (ctypes.c_int32 * 5)()
+    grid = lib.seco_debug_fwd_schedule(ctypes.byref(s), j, sms, out)
+    return grid, dict(zip(("pair", "units", "n_full", "nsplit", "merge"), list(out)))
+
+
+def test_forward_split_plan_policy(lib):
+    """The forward's work plan (seco_debug_fwd_schedule, host only): cfg3 runs the
+    CTA-pair kernel on 128 pair-units, whole for j < 10 and DP + split tail from j = 10 (74
+    whole units, then 4 key-range pieces of the other 54, merged in-kernel); the 8-rank per-rank
+    shape (4 q / 1 kv heads) is a sub-wave grid, split into pieces merged by the combine kernel;
+    chunk 0 never splits; every plan's grid covers its work items exactly."""
+    for j in range(16):
+        grid, p = _fwd_plan(lib, 32, 8, 2048, 16, j)
+        assert p["pair"] == 1 and p["units"] == 128
+        if j < 10:
+            assert p["nsplit"] == 1 and p["n_full"] == 128 and p["merge"] == 0 and grid == 256
+        else:
+            assert p == dict(pair=1, units=128, n_full=74, nsplit=4, merge=1)
+            assert grid == 2 * (74 + 54 * 4)
+    for j in range(16):
+        grid, p = _fwd_plan(lib, 4, 1, 2048, 16, j)
+        assert p["pair"] == 0 and p["units"] == 32 and p["n_full"] in (0, 32)
+        if j == 0:
+            assert p["nsplit"] == 1 and grid == 32
+        else:
+            assert p["nsplit"] > 1 and p["merge"] == 0 and p["n_full"] == 0 and grid == 32 * p["nsplit"]
+            assert (j * 2048 // 128 + 1) >= 8 * p["nsplit"]          # >= 8 K/V tiles per piece
+    # ragged chunks: ceil(c / 128) query tiles per chunk
+    grid, p = _fwd_plan(lib, 8, 2, 1000, 4, 3)
+    assert p["units"] == 8 * 4 and p["n_full"] == 0 and grid == 32 * p["nsplit"]
+    # a pretended 5-SM GPU: multi-wave grids at small shapes take the DP + tail form
+    grid, p = _fwd_plan(lib, 8, 2, 1024, 4, 3, sms=5)
+    assert p["merge"] == 1 and p["n_full"] == 30 and grid == p["n_full"] + (p["units"] - p["n_full"]) * p["nsplit"]
+    assert lib.seco_debug_fwd_schedule(ctypes.byref(_shape()), 9, 0, (ctypes.c_int32 * 5)()) == -1   # j out of range
